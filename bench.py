@@ -1,0 +1,368 @@
+#!/usr/bin/env python3
+"""Benchmark driver (replaces the reference's proj/benchmarks/bench.cpp).
+
+Workload (BASELINE config 4): Jacobi-2D 5-point, fp64, 32768 x 32768 per GPU,
+T = 512 steps, zero Dirichlet ring, F = init_value("F", flat) (reference
+exec.cpp:21-28).  One "step" = one full T=512 run of the hot path.
+  --gpus N (torchrun, one rank per GPU): rows are sharded; weak scaling keeps
+  32768 rows per rank (global grid 32768N x 32768), halo rows exchanged with
+  NCCL send/recv every bt steps, overlapped with the interior.
+
+Metric: stencil GUpdates/s (whole job), plus
+  roofline  — dominant kernel s2d5 (16 algorithmic bytes per cell per launch,
+              i.e. 16/bt B/update) vs the measured HBM copy bandwidth;
+  e2e       — the same metric through the C ABI (pcotgpu_write_array(F) from
+              pinned host memory -> pcotgpu_run -> pcotgpu_read_array(Out));
+  cpu_baseline — the reference's own tiled CPU path (its emitted C, OpenMP,
+              all host cores) on a bounded sample, rank 0, N=1.
+--impl reference runs only that reference CPU path (rank 0) on the sample.
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+EMIT_DIR = os.path.join(REPO, "oracle", "_ref", "emit")
+SAMPLE = "jacobi2d_N8192_T32"
+SAMPLE_INIT = "jacobi2d_N8192_T0"
+SAMPLE_UPDATES = 8192 * 8192 * 32
+METRIC = "stencil GUpdates/s"
+
+
+def env_rank():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
+            int(os.environ.get("LOCAL_RANK", 0)))
+
+
+def peak_hbm():
+    p = os.path.join(REPO, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def ncu_traffic():
+    """dram bytes per s2d5 launch from the committed ncu --set full summary."""
+    p = os.path.join(REPO, "profiles", "ncu_s2d5_summary.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return d.get("dram_bytes_per_launch_scaled_to_bench")
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.path = None
+
+    def __enter__(self):
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), "--query-gpu=" + q,
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            self.proc.wait()
+
+    def summary(self):
+        sms, mx, reasons = [], None, set()
+        try:
+            for line in open(self.path):
+                f = [x.strip() for x in line.split(",")]
+                if len(f) < 9:
+                    continue
+                sms.append(float(f[1]))
+                mx = float(f[2])
+                names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+                for n, v in zip(names, f[5:9]):
+                    if v.lower().startswith("active"):
+                        reasons.add(n)
+        except Exception:
+            pass
+        finally:
+            try:
+                os.unlink(self.path)
+            except OSError:
+                pass
+        return {"sm_mhz": statistics.median(sms) if sms else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sms)}
+
+
+def run_reference_sample(threads):
+    """Wall time of the reference's emitted C on the sample minus its init-only twin."""
+    env = dict(os.environ)
+    env["OMP_NUM_THREADS"] = str(threads)
+
+    def wall(tag):
+        b = os.path.join(EMIT_DIR, tag)
+        t0 = time.perf_counter()
+        out = subprocess.run([b], capture_output=True, text=True, env=env, check=True)
+        return time.perf_counter() - t0, out.stdout.split()[1]
+
+    t_init, _ = wall(SAMPLE_INIT)
+    t_run, chk = wall(SAMPLE)
+    return max(t_run - t_init, 1e-9), chk
+
+
+def cpu_baseline_port(threads):
+    """Fallback when oracle/_ref was not shipped: the oracle port on the sample."""
+    from tests import oracle_ctypes as O
+
+    O.lib().oracle_set_threads(threads)
+    F = O.init_array("F", 8192 * 8192)
+    t0 = time.perf_counter()
+    O.stencil2d5(8192, 32, 0, F)
+    return time.perf_counter() - t0
+
+
+def reference_available():
+    return os.path.exists(os.path.join(EMIT_DIR, SAMPLE)) and os.path.exists(
+        os.path.join(EMIT_DIR, SAMPLE_INIT))
+
+
+def cpu_baseline(threads):
+    if reference_available():
+        secs, chk = run_reference_sample(threads)
+        kind = "reference"
+    else:
+        secs, chk = cpu_baseline_port(threads), None
+        kind = "port"
+    return {"value": SAMPLE_UPDATES / secs / 1e9, "unit": "GUpdates/s", "cores": threads,
+            "kind": kind, "seconds": round(secs, 3), "checksum": chk,
+            "sample": "Jacobi-2D 8192^2, T=32 (same rule/ring/init as config 4; "
+                      "reference emitted recursive C, OpenMP tasks, -O2 -ffp-contract=off; "
+                      "wall minus init-only run)"}
+
+
+def reference_arm(args, rank, world):
+    if rank != 0:
+        return 0
+    threads = os.cpu_count() or 1
+    times = []
+    kind = "reference" if reference_available() else "port"
+    for i in range(args.warmup + args.steps):
+        if kind == "reference":
+            secs, _ = run_reference_sample(threads)
+        else:
+            secs = cpu_baseline_port(threads)
+        if i >= args.warmup:
+            times.append(secs)
+    ms = 1000.0 * sum(times) / len(times)
+    value = SAMPLE_UPDATES / (ms / 1000.0) / 1e9
+    line = {
+        "metric": METRIC, "value": value, "unit": "GUpdates/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (reference init_value)", "impl": "reference",
+        "config": {"workload": "jacobi2d 8192x8192 T=32 (bounded CPU sample of config 4)",
+                   "parallelism": "OpenMP tasks, %d threads" % threads},
+        "cpu_baseline": {"value": value, "unit": "GUpdates/s", "cores": threads, "kind": kind,
+                         "sample": "Jacobi-2D 8192^2 T=32, reference emitted C"},
+        "e2e": {"value": value, "unit": "GUpdates/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--rows", type=int, default=32768, help="rows per rank (weak scaling)")
+    ap.add_argument("--cols", type=int, default=32768)
+    ap.add_argument("--T", type=int, default=512)
+    ap.add_argument("--bt", type=int, default=int(os.environ.get("PCOTGPU_BT2D", 6)))
+    ap.add_argument("--scheme", default="slt", choices=["slt", "cot"])
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    rank, world, local = env_rank()
+
+    if args.impl == "reference":
+        return reference_arm(args, rank, world)
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_1802_00166_b200 as P
+    from paper_1802_00166_b200.sharded import ShardedStencil2D
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    rows = args.rows if args.scaling == "weak" else args.rows // world
+    S = ShardedStencil2D(rows, args.cols, args.T, args.bt, ring_hold=0,
+                         order=0 if args.scheme == "slt" else 1, device=dev)
+    S.fill_init("F")
+    S.snapshot_input()
+    torch.cuda.synchronize()
+
+    def barrier():
+        if world > 1:
+            dist.barrier(device_ids=[local])
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        S.restart()  # every step restarts from F (copy of the step-0 slab, inside the step)
+        S.run()
+    barrier()
+    stream = torch.cuda.current_stream(dev)
+    l0 = P.lib().pcotgpu_launch_count()
+    S.kernel_events.clear()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clocks:
+        barrier()
+        e0.record(stream)
+        for _ in range(args.steps):
+            S.restart()
+            S.run(record=True)
+        e1.record(stream)
+        barrier()
+    launches = P.lib().pcotgpu_launch_count() - l0
+    ms = e0.elapsed_time(e1) / args.steps
+    kms = [a.elapsed_time(b) for a, b in S.kernel_events]
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    updates = float(rows) * args.cols * args.T * world
+    value = updates / (ms_max / 1e3) / 1e9
+
+    # roofline of the dominant kernel: 16 B per cell per launch (one read + one write)
+    cells = float(rows) * args.cols
+    blocks = -(-args.T // args.bt)
+    bytes_per_run = 16.0 * cells * blocks
+    kernel_ms = sum(kms) / args.steps  # summed launch time per step
+    peak, peak_src = peak_hbm()
+    achieved = bytes_per_run / (kernel_ms / 1e3) / 1e9 if kernel_ms > 0 else None
+    traffic = ncu_traffic()
+    roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+            "frac": (achieved / peak) if achieved else None, "traffic": traffic,
+            "kernel": "s2d5_kernel<bt=%d>" % args.bt, "peak_source": peak_src,
+            "avg_launch_ms": (sum(kms) / len(kms)) if kms else None,
+            "launches_per_step": len(kms) // max(1, args.steps),
+            "bytes_per_update": 16.0 / args.bt, "kernel_share_of_step": kernel_ms / ms if ms else None}
+
+    # e2e through the C ABI with host buffers (N=1: GpuExecutor; N>1: slab copies)
+    e2e = None
+    if not args.no_e2e:
+        e2e = measure_e2e(args, P, torch, dist, S, dev, world, rows, updates, local)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(os.cpu_count() or 1)
+
+    if rank == 0:
+        cl = clocks.summary()
+        line = {
+            "metric": METRIC, "value": value, "unit": "GUpdates/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max,
+            "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic (reference init_value seeds, on device)",
+            "config": {"workload": "jacobi2d (BASELINE config 4): %dx%d per rank, T=%d, zero ring"
+                                   % (rows, args.cols, args.T),
+                       "global_grid": [rows * world, args.cols], "T": args.T, "bt": args.bt,
+                       "tile_order": args.scheme, "parallelism": "row-shard x%d" % world,
+                       "halo": "NCCL send/recv of bt rows every bt steps, overlapped" if world > 1 else None,
+                       "l2": "inputs larger than L2 (two %.1f GiB slabs per rank)" % (cells * 8 / 2**30)},
+            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
+            "clocks": {"sm_mhz": cl["sm_mhz"], "sm_max_mhz": cl["sm_max_mhz"], "reasons": cl["reasons"]},
+            "fp64_updates_per_step": updates,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def measure_e2e(args, P, torch, dist, S, dev, world, rows, updates, local):
+    """Inputs start in pinned host memory; every step copies F in, runs, copies Out back."""
+    import numpy as np
+
+    n_cells = rows * args.cols
+    # host copy of this rank's F, produced by the device generator once (untimed)
+    host_F = torch.empty(n_cells, dtype=torch.float64, pin_memory=True)
+    host_out = torch.empty(n_cells, dtype=torch.float64, pin_memory=True)
+    stream = torch.cuda.current_stream(dev)
+    if world == 1 and rows == args.cols:
+        ex = P.GpuExecutor("jacobi2d", {"T": args.T, "N": rows}, device=local)
+        ex.set_stream(stream.cuda_stream)
+        F_np = host_F.numpy()
+        ex.array_data("F", out=F_np)
+        out_np = host_out.numpy()
+        sched = ("slt" if args.scheme == "slt" else "cot", [args.bt, 64, 256])
+
+        def step():
+            ex.write_array("F", F_np)
+            ex.run(*sched, skip_checksum=True)
+            ex.array_data("Out", out=out_np)
+    else:
+        S.restart()
+        host_F.copy_(S.interior(0).reshape(-1))
+        torch.cuda.synchronize()
+
+        def step():
+            S.interior(0).copy_(host_F.view(rows, args.cols), non_blocking=True)
+            S.exchange_sync(0)
+            S.cur = 0
+            S.run()
+            host_out.view(rows, args.cols).copy_(S.interior(S.cur), non_blocking=True)
+    for _ in range(1):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier(device_ids=[local])
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    steps = max(1, min(args.steps, 2))
+    e0.record(stream)
+    for _ in range(steps):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    return {"value": updates / (ms / 1e3) / 1e9, "unit": "GUpdates/s",
+            "h2d_bytes_per_step": n_cells * 8, "d2h_bytes_per_step": n_cells * 8,
+            "ms_per_step": ms, "steps": steps,
+            "path": "C ABI pcotgpu_write_array -> pcotgpu_run -> pcotgpu_read_array"
+                    if world == 1 else "pinned host slab copies + sharded run"}
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -106,6 +106,78 @@ def jacobi2d():
     return spec("jacobi2d", ["T", "N"], ["t", "x", "y"], {"T": 3, "N": 6}, arrays, sts)
 
 
+def heat2d_hold():
+    """Same semantics as the reference corpus heat2d (kernels/heat2d.kernel):
+    t=0 copies all of F, the ring is copied forward from step t-1 (so it keeps
+    F's values), interior gets the 5-point body.  Written independently here
+    so the GPU test-suite does not need the reference tree; make_golden.py
+    checks that the reference interpreter gives both specs the same checksum.
+    """
+    s = Space(["t", "x", "y"], ["T", "N"])
+    i = lin((1, "x"), (-1, "t"))
+    j = lin((1, "y"), (-1, "t"))
+    N1, N2 = lin((1, "N"), const=-1), lin((1, "N"), const=-2)
+    t_up = s.between(lin((1, "t")), C(1), lin((1, "T")))
+    t0 = s.eq(lin((1, "t")), C(0))
+    i_in, j_in = s.between(i, C(1), N2), s.between(j, C(1), N2)
+    i_all, j_all = s.between(i, C(0), N1), s.between(j, C(0), N1)
+    subs = ["t", "x", "y"]
+    cp = "X[t - 1, x - 1, y - 1]"
+    sts = [
+        stmt("S0", 3, t0 + i_all + j_all, "X", subs, "F[x, y]"),
+        stmt("S1", 3, t_up + i_in + j_in, "X", subs,
+             "0.2 * (X[t - 1, x - 1, y - 1] + X[t - 1, x - 2, y - 1] + "
+             "X[t - 1, x, y - 1] + X[t - 1, x - 1, y - 2] + X[t - 1, x - 1, y])"),
+        stmt("C0", 3, t_up + s.eq(i, C(0)) + j_all, "X", subs, cp),
+        stmt("C1", 3, t_up + s.eq(i, N1) + j_all, "X", subs, cp),
+        stmt("C2", 3, t_up + i_in + s.eq(j, C(0)), "X", subs, cp),
+        stmt("C3", 3, t_up + i_in + s.eq(j, N1), "X", subs, cp),
+        stmt("Sfin", 3, s.eq(lin((1, "t")), lin((1, "T"))) + i_all + j_all, "Out",
+             ["x - T", "y - T"], "X[t, x, y]"),
+    ]
+    arrays = [
+        {"name": "F", "rank": 2, "extents": ["N", "N"], "kind": "input"},
+        {"name": "X", "rank": 3, "extents": ["T + 1", "N + T", "N + T"], "kind": "temp"},
+        {"name": "Out", "rank": 2, "extents": ["N", "N"], "kind": "output"},
+    ]
+    return spec("heat2d_hold", ["T", "N"], ["t", "x", "y"], {"T": 3, "N": 6}, arrays, sts)
+
+
+def heat3d_hold():
+    """Same semantics as the reference corpus heat3d (kernels/heat3d.kernel:34):
+    0.1 * (c + 6 neighbours), ring copied forward from step t-1."""
+    s = Space(["t", "x", "y", "w"], ["T", "N"])
+    i = lin((1, "x"), (-1, "t"))
+    j = lin((1, "y"), (-1, "t"))
+    k = lin((1, "w"), (-1, "t"))
+    N1, N2 = lin((1, "N"), const=-1), lin((1, "N"), const=-2)
+    t_up = s.between(lin((1, "t")), C(1), lin((1, "T")))
+    t0 = s.eq(lin((1, "t")), C(0))
+    inn = [s.between(v, C(1), N2) for v in (i, j, k)]
+    alll = [s.between(v, C(0), N1) for v in (i, j, k)]
+    subs = ["t", "x", "y", "w"]
+    c = "X[t - 1, x - 1, y - 1, w - 1]"
+    body = ("0.1 * (" + c + " + X[t - 1, x - 2, y - 1, w - 1] + X[t - 1, x, y - 1, w - 1] + "
+            "X[t - 1, x - 1, y - 2, w - 1] + X[t - 1, x - 1, y, w - 1] + "
+            "X[t - 1, x - 1, y - 1, w - 2] + X[t - 1, x - 1, y - 1, w])")
+    sts = [stmt("S0", 4, t0 + alll[0] + alll[1] + alll[2], "X", subs, "F[x, y, w]"),
+           stmt("S1", 4, t_up + inn[0] + inn[1] + inn[2], "X", subs, body)]
+    n = 0
+    for v, rest in ((i, alll[1] + alll[2]), (j, inn[0] + alll[2]), (k, inn[0] + inn[1])):
+        for val in (C(0), N1):
+            sts.append(stmt("C%d" % n, 4, t_up + s.eq(v, val) + rest, "X", subs, c))
+            n += 1
+    sts.append(stmt("Sfin", 4, s.eq(lin((1, "t")), lin((1, "T"))) + alll[0] + alll[1] + alll[2],
+                    "Out", ["x - T", "y - T", "w - T"], "X[t, x, y, w]"))
+    arrays = [
+        {"name": "F", "rank": 3, "extents": ["N", "N", "N"], "kind": "input"},
+        {"name": "X", "rank": 4, "extents": ["T + 1", "N + T", "N + T", "N + T"],
+         "kind": "temp"},
+        {"name": "Out", "rank": 3, "extents": ["N", "N", "N"], "kind": "output"},
+    ]
+    return spec("heat3d_hold", ["T", "N"], ["t", "x", "y", "w"], {"T": 2, "N": 5}, arrays, sts)
+
+
 # ---------------------------------------------------------------- heat3d_b
 def heat3d_b():
     """Heat-3D 7-point with the BASELINE rule c + 0.125*(sum6 - 6c), zero ring.
@@ -220,7 +292,7 @@ def dump(obj):
 
 
 def main():
-    for fn in (jacobi2d, heat3d_b, gs2d, gemm):
+    for fn in (jacobi2d, heat2d_hold, heat3d_hold, heat3d_b, gs2d, gemm):
         k = fn()
         path = os.path.join(HERE, k["name"] + ".kernel")
         with open(path, "w") as f:

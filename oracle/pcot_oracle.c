@@ -51,6 +51,19 @@ double oracle_init_value(const char* name, uint64_t flat) {
   return (double)(splitmix_from(h, flat) >> 11) * 0x1.0p-53;
 }
 
+/* init_value over a window [r0, r0+h) x [c0, c0+w) of a row-major grid with
+ * `ncols` columns (flat = r*ncols + c), written densely to out[h*w]. */
+void oracle_init_window(const char* name, uint64_t ncols, uint64_t r0, uint64_t c0, uint64_t h,
+                        uint64_t w, double* out) {
+  uint64_t hs = oracle_fnv1a(name, strlen(name), 0xcbf29ce484222325ULL);
+  int nt = oracle_get_threads();
+#pragma omp parallel for num_threads(nt) schedule(static)
+  for (int64_t r = 0; r < (int64_t)h; ++r)
+    for (uint64_t c = 0; c < w; ++c)
+      out[(uint64_t)r * w + c] =
+          (double)(splitmix_from(hs, (r0 + (uint64_t)r) * ncols + c0 + c) >> 11) * 0x1.0p-53;
+}
+
 void oracle_init_array(const char* name, double* out, uint64_t n) {
   uint64_t h = oracle_fnv1a(name, strlen(name), 0xcbf29ce484222325ULL);
   int nt = oracle_get_threads();

@@ -1,0 +1,79 @@
+// Shared device helpers for the sm_100a hot-path kernels.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#define PCOT_DEV __device__ __forceinline__
+
+namespace pcotgpu {
+
+// ---------------------------------------------------------------- fp64, exact
+// Every stencil update is written with explicit round-to-nearest intrinsics so
+// no FMA contraction can change a bit (reference exec.cpp:347-428 evaluates
+// one rounding per operation; emitted C is built -ffp-contract=off).
+PCOT_DEV double add(double a, double b) { return __dadd_rn(a, b); }
+PCOT_DEV double sub(double a, double b) { return __dsub_rn(a, b); }
+PCOT_DEV double mul(double a, double b) { return __dmul_rn(a, b); }
+PCOT_DEV double div(double a, double b) { return __ddiv_rn(a, b); }
+
+// ---------------------------------------------------------------- mbarrier + bulk copy (TMA engine)
+PCOT_DEV uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+PCOT_DEV void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+PCOT_DEV void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+PCOT_DEV void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+PCOT_DEV void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+
+PCOT_DEV bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+      " selp.u32 %0, 1, 0, p;\n}\n"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+
+PCOT_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
+  while (!mbar_try_wait(bar, parity)) {
+  }
+}
+
+// 1-D bulk copy global -> shared through the TMA engine, completion counted on
+// an mbarrier (SASS: UBLKCP).  src/dst 16-B aligned, bytes a multiple of 16.
+PCOT_DEV void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// ---------------------------------------------------------------- acquire/release flags
+PCOT_DEV int ld_acquire(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+PCOT_DEV void st_release(int* p, int v) {
+  asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+PCOT_DEV double ld_cg(const double* p) { return __ldcg(p); }
+
+}  // namespace pcotgpu

@@ -1,0 +1,224 @@
+// In-place Gauss-Seidel 9-point, skewed tile wavefront, sm_100a.
+//
+// Replaces exec_stmt over kernels/gs2d.kernel (reference core/src/exec.cpp:
+// 347-428) under the in-place storage allocate() derives for it (UOV (1,1,2),
+// map (t mod 1, x-t, y-2t): reference memalloc.cpp:542-595).
+//
+// Tiles are boxes in the kernel's skewed band (t, x = t+i, y = 2t+i+j), where
+// every dependence is non-negative (reference tilable_band semantics,
+// tiler.cpp:189-243), so a tile only waits for its <= 7 lower neighbours.
+// A persistent grid pulls tiles from a global queue in wavefront order and
+// spins (acquire) on the predecessors' completion flags — no grid-wide sync.
+// Inside a tile, thread (tt, xx) owns the line (t0+tt, x0+xx) and sweeps y;
+// clock h = t + x + y (= 4t + 2i + j) is a legal point schedule: every
+// dependence distance has positive coordinate sum, so one __syncthreads per
+// clock orders the whole tile.  The tile's cells live in shared memory in the
+// reference's storage coordinates (i, s = i + j); global memory is written
+// through, and the universal occupancy vector makes any dependence-respecting
+// concurrent tile schedule safe for in-place storage.
+// Per point: 3x3 in row-major order, left-associated sum, IEEE '/ 9.0'.
+#include <algorithm>
+#include <map>
+#include <tuple>
+#include <vector>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace pcotgpu {
+
+struct GsPlan {
+  int64_t n = 0, T = 0;
+  int bt = 0, bx = 0, by = 0;
+  int64_t ntiles = 0;
+  int grid = 0;
+  int* d_tiles = nullptr;   // [ntiles][3]: tb, xb, yb
+  int* d_preds = nullptr;   // [ntiles][8]: predecessor tile ids (-1 = none)
+  int* d_state = nullptr;   // [ntiles] flags + [1] queue counter
+  int device = 0;
+};
+
+namespace {
+
+struct GsArgs {
+  double* a;
+  int64_t ld, n, T;
+  int bt, bx, by;
+  int ni, ns;  // smem region rows / cols
+  int64_t ntiles;
+  const int* tiles;
+  const int* preds;
+  int* flags;
+  int* counter;
+};
+
+__global__ void gs2d_kernel(GsArgs g) {
+  extern __shared__ __align__(16) double reg[];
+  __shared__ int s_tile;
+  const int tid = threadIdx.x;
+  const int nthr = g.bt * g.bx;
+  for (;;) {
+    if (tid == 0) s_tile = atomicAdd(g.counter, 1);
+    __syncthreads();
+    const int tile = s_tile;
+    if (tile >= g.ntiles) return;
+    const int tb = g.tiles[tile * 3 + 0], xb = g.tiles[tile * 3 + 1], yb = g.tiles[tile * 3 + 2];
+    if (tid < 8) {
+      const int p = g.preds[tile * 8 + tid];
+      if (p >= 0)
+        while (ld_acquire(g.flags + p) == 0) __nanosleep(64);
+    }
+    __syncthreads();
+    const int64_t t0 = 1 + int64_t(tb) * g.bt;
+    const int64_t x0 = 2 + int64_t(xb) * g.bx;
+    const int64_t y0 = 4 + int64_t(yb) * g.by;
+    // region: i in [I0, I0+ni), s = i+j in [S0, S0+ns)
+    const int64_t I0 = x0 - t0 - g.bt;
+    const int64_t S0 = y0 - 2 * t0 - 2 * g.bt;
+    for (int r = tid / 32; r < g.ni; r += nthr / 32) {
+      const int64_t i = I0 + r;
+      for (int c = tid % 32; c < g.ns; c += 32) {
+        const int64_t j = S0 + c - i;
+        double v = 0.0;
+        if (i >= 0 && i < g.n && j >= 0 && j < g.n) v = ld_cg(g.a + i * g.ld + j);
+        reg[r * g.ns + c] = v;
+      }
+    }
+    __syncthreads();
+    const int tt = tid / g.bx, xx = tid - (tid / g.bx) * g.bx;
+    const int64_t t = t0 + tt, x = x0 + xx, i = x - t;
+    const bool line_ok = t <= g.T && i >= 1 && i <= g.n - 2;
+    const int nclk = g.bt + g.bx + g.by - 2;
+    const int ri = int(i - I0);
+    for (int clk = 0; clk < nclk; ++clk) {
+      const int yy = clk - tt - xx;
+      if (line_ok && yy >= 0 && yy < g.by) {
+        const int64_t y = y0 + yy;
+        const int64_t s = y - 2 * t;
+        const int64_t j = s - i;
+        if (j >= 1 && j <= g.n - 2) {
+          const int cs = int(s - S0);
+          const double* up = reg + (ri - 1) * g.ns + cs;
+          double* me = reg + ri * g.ns + cs;
+          const double* dn = reg + (ri + 1) * g.ns + cs;
+          double acc = add(up[-2], up[-1]);
+          acc = add(acc, up[0]);
+          acc = add(acc, me[-1]);
+          acc = add(acc, me[0]);
+          acc = add(acc, me[1]);
+          acc = add(acc, dn[0]);
+          acc = add(acc, dn[1]);
+          acc = add(acc, dn[2]);
+          const double v = div(acc, 9.0);
+          me[0] = v;
+          g.a[i * g.ld + j] = v;
+        }
+      }
+      __syncthreads();
+    }
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) st_release(g.flags + tile, 1);
+  }
+}
+
+}  // namespace
+
+GsPlan* gs2d_plan_create(int64_t n, int64_t T, int bt, int bx, int by, int device) {
+  GsPlan* p = new GsPlan;
+  p->n = n;
+  p->T = T;
+  p->bt = bt;
+  p->bx = bx;
+  p->by = by;
+  p->device = device;
+  if (T < 1 || n < 3) return p;  // nothing to do
+  const int64_t NT = (T + bt - 1) / bt;
+  const int64_t xmax = T + n - 2, ymax = 2 * T + 2 * (n - 2);
+  const int64_t NX = (xmax - 2) / bx + 1, NY = (ymax - 4) / by + 1;
+  // Non-empty tiles (exact test per line), then wavefront order.
+  std::vector<std::tuple<int64_t, int, int, int>> order;
+  std::map<std::tuple<int, int, int>, int> idx;
+  auto nonempty = [&](int64_t tb, int64_t xb, int64_t yb) {
+    for (int64_t t = 1 + tb * bt; t < 1 + (tb + 1) * bt && t <= T; ++t) {
+      const int64_t xlo = 2 + xb * bx, xhi = xlo + bx - 1;
+      const int64_t ilo = std::max<int64_t>(1, xlo - t), ihi = std::min<int64_t>(n - 2, xhi - t);
+      if (ilo > ihi) continue;
+      const int64_t ylo = 4 + yb * by, yhi = ylo + by - 1;
+      // y = 2t + i + j, j in [1, n-2], i in [ilo, ihi]
+      const int64_t ymin = 2 * t + ilo + 1, ymax2 = 2 * t + ihi + n - 2;
+      if (std::max(ylo, ymin) <= std::min(yhi, ymax2)) return true;
+    }
+    return false;
+  };
+  for (int64_t tb = 0; tb < NT; ++tb)
+    for (int64_t xb = 0; xb < NX; ++xb)
+      for (int64_t yb = 0; yb < NY; ++yb)
+        if (nonempty(tb, xb, yb)) order.emplace_back(tb + xb + yb, int(tb), int(xb), int(yb));
+  std::sort(order.begin(), order.end());
+  std::vector<int> tiles, preds;
+  for (size_t q = 0; q < order.size(); ++q) {
+    auto [w, tb, xb, yb] = order[q];
+    idx[{tb, xb, yb}] = int(q);
+    tiles.insert(tiles.end(), {tb, xb, yb});
+    int np = 0;
+    int pr[8] = {-1, -1, -1, -1, -1, -1, -1, -1};
+    for (int m = 1; m < 8; ++m) {
+      auto it = idx.find({tb - (m >> 2 & 1), xb - (m >> 1 & 1), yb - (m & 1)});
+      if (it != idx.end()) pr[np++] = it->second;
+    }
+    preds.insert(preds.end(), pr, pr + 8);
+  }
+  p->ntiles = int64_t(order.size());
+  cudaSetDevice(device);
+  cudaMalloc(&p->d_tiles, tiles.size() * sizeof(int));
+  cudaMalloc(&p->d_preds, preds.size() * sizeof(int));
+  cudaMalloc(&p->d_state, (p->ntiles + 1) * sizeof(int));
+  cudaMemcpy(p->d_tiles, tiles.data(), tiles.size() * sizeof(int), cudaMemcpyHostToDevice);
+  cudaMemcpy(p->d_preds, preds.data(), preds.size() * sizeof(int), cudaMemcpyHostToDevice);
+  const int ni = bx + bt + 1, ns = by + 2 * bt + 2;
+  const size_t smem = size_t(ni) * ns * 8;
+  cudaFuncSetAttribute(gs2d_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  int occ = 0, sms = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, gs2d_kernel, bt * bx, smem);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+  p->grid = int(std::max<int64_t>(1, std::min<int64_t>(p->ntiles, int64_t(occ) * sms)));
+  return p;
+}
+
+void gs2d_plan_destroy(GsPlan* p) {
+  if (!p) return;
+  cudaFree(p->d_tiles);
+  cudaFree(p->d_preds);
+  cudaFree(p->d_state);
+  delete p;
+}
+
+int64_t gs2d_plan_tiles(const GsPlan* p) { return p ? p->ntiles : 0; }
+
+cudaError_t gs2d_run(GsPlan* p, double* a, int64_t ld, cudaStream_t stream) {
+  if (p->ntiles == 0) return cudaSuccess;
+  cudaError_t e = cudaMemsetAsync(p->d_state, 0, (p->ntiles + 1) * sizeof(int), stream);
+  if (e != cudaSuccess) return e;
+  GsArgs g;
+  g.a = a;
+  g.ld = ld;
+  g.n = p->n;
+  g.T = p->T;
+  g.bt = p->bt;
+  g.bx = p->bx;
+  g.by = p->by;
+  g.ni = p->bx + p->bt + 1;
+  g.ns = p->by + 2 * p->bt + 2;
+  g.ntiles = p->ntiles;
+  g.tiles = p->d_tiles;
+  g.preds = p->d_preds;
+  g.flags = p->d_state;
+  g.counter = p->d_state + p->ntiles;
+  const size_t smem = size_t(g.ni) * g.ns * 8;
+  gs2d_kernel<<<p->grid, p->bt * p->bx, smem, stream>>>(g);
+  count_launch();
+  return cudaGetLastError();
+}
+
+}  // namespace pcotgpu

@@ -1,0 +1,78 @@
+// Internal launch interface of the sm_100a kernels (host side, no torch types).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace pcotgpu {
+
+// Row-sharded 2-D grid slab.  `origin` points at local cell (0,0); rows
+// [-ghost, R+ghost) and columns [-padl, ld-padl) are addressable.
+struct Slab2D {
+  double* origin = nullptr;
+  int64_t ld = 0;       // row pitch in doubles (multiple of 16)
+  int64_t rows = 0;     // R, local rows owned
+  int64_t cols = 0;     // N, grid columns
+  int64_t ghost = 0;    // ghost rows above and below
+  int64_t padl = 0;     // addressable columns left of column 0
+};
+
+enum TileOrderMode { kOrderLex = 0, kOrderMorton = 1 };
+
+// Advance a 2-D 5-point slab by `bt` steps (1 <= bt <= 8): out = S^bt(in) on
+// local rows [0, R).  Rows [-bt, 0) and [R, R+bt) of `in` must hold step-t0
+// values of the neighbouring rows (ghost rows; ignored outside the grid).
+// g0 = global row of local row 0; nrows = global row count (ring detection).
+// ring_hold: 0 -> ring cells are 0.0 (jacobi2d.kernel), 1 -> ring cells keep
+// their value (reference heat2d.kernel S2-S5).
+cudaError_t s2d5_advance(const Slab2D& in, const Slab2D& out, int64_t g0, int64_t nrows,
+                         int bt, int ring_hold, int order, int row_lo, int row_hi,
+                         cudaStream_t stream);
+int s2d5_max_bt();
+
+// 3-D 7-point, dense N^3 cube with halo padding (see Grid3D).
+struct Grid3D {
+  double* origin = nullptr;  // cell (0,0,0)
+  int64_t n = 0;             // N
+  int64_t pitch_j = 0;       // doubles between j rows (multiple of 16)
+  int64_t pitch_i = 0;       // doubles between i planes
+  int64_t halo = 0;          // addressable halo planes/rows/cols on each side
+};
+// rule 0: c + 0.125*(sum6 - 6c) (heat3d_b); rule 1: 0.1*(c + sum6) (heat3d).
+cudaError_t s3d7_advance(const Grid3D& in, const Grid3D& out, int bt, int rule, int ring_hold,
+                         int order, cudaStream_t stream);
+int s3d7_max_bt();
+
+// In-place Gauss-Seidel 9-point, T sweeps, tile wavefront.  `a` is an N x N
+// row-major array with pitch `ld` (ring cells fixed at their value).
+struct GsPlan;  // host-side tile plan (device buffers owned by the plan)
+GsPlan* gs2d_plan_create(int64_t n, int64_t T, int bt, int bx, int by, int device);
+void gs2d_plan_destroy(GsPlan* p);
+cudaError_t gs2d_run(GsPlan* p, double* a, int64_t ld, cudaStream_t stream);
+int64_t gs2d_plan_tiles(const GsPlan* p);
+
+// C = A*B, fp64 DMMA tensor cores, row-major N x N with pitch ld.
+cudaError_t dgemm_nn(const double* A, const double* B, double* C, int64_t n, int64_t ld,
+                     int order, cudaStream_t stream);
+// y = 2x - 1 elementwise (exact for x in [0,1) of the reference init_value).
+cudaError_t affine_2x_minus_1(const double* x, double* y, int64_t count, cudaStream_t stream);
+
+// Reference init_value (exec.cpp:21-28) on device: dst[r*ld + c] =
+// init_value(name, flat0 + r*ncols + c) for r < nrows, c < ncols.
+cudaError_t fill_init_value(double* dst, int64_t ld, int64_t nrows, int64_t ncols,
+                            uint64_t name_hash, uint64_t flat0, cudaStream_t stream);
+// 3-D variant over an N^3 cube with pitches.
+cudaError_t fill_init_value_3d(const Grid3D& g, uint64_t name_hash, cudaStream_t stream);
+// Copy a dense row-major [nrows x ncols] block between pitched layouts.
+// With plane pitches (pd, rows_per_plane) the destination row r lands at
+// plane r / rows_per_plane, row r % rows_per_plane (dense source).
+cudaError_t copy_rows(double* dst, int64_t ldd, const double* src, int64_t lds, int64_t nrows,
+                      int64_t ncols, cudaStream_t stream, int64_t pd = 0, int64_t rows_per_plane = 0);
+// Zero (or keep) the ring of a 2-D grid: cells on rows 0/N-1, cols 0/N-1.
+cudaError_t zero_ring_2d(double* origin, int64_t ld, int64_t n, cudaStream_t stream);
+cudaError_t zero_ring_3d(const Grid3D& g, cudaStream_t stream);
+
+// Launch counter (every kernel launched by this library increments it).
+uint64_t launches();
+void count_launch(uint64_t n = 1);
+
+}  // namespace pcotgpu

@@ -1,0 +1,128 @@
+// Device utilities: the reference's deterministic input generator, pitched
+// copies, ring reset, and the launch counter.
+#include <atomic>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace pcotgpu {
+
+namespace {
+
+std::atomic<uint64_t> g_launches{0};
+
+// reference exec.cpp:21-28: splitmix64(fnv1a(name) ^ flat*phi) >> 11, * 2^-53
+PCOT_DEV double init_value_dev(uint64_t h, uint64_t flat) {
+  uint64_t x = h ^ (flat * 0x9E3779B97F4A7C15ULL);
+  x += 0x9E3779B97F4A7C15ULL;
+  x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ULL;
+  x = (x ^ (x >> 27)) * 0x94D049BB133111EBULL;
+  x ^= x >> 31;
+  return double(x >> 11) * 0x1.0p-53;  // exact: 53-bit integer times a power of two
+}
+
+__global__ void fill2d_kernel(double* dst, int64_t ld, int64_t nrows, int64_t ncols, uint64_t h,
+                              uint64_t flat0) {
+  const int64_t total = nrows * ncols;
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < total;
+       e += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t r = e / ncols, c = e - r * ncols;
+    dst[r * ld + c] = init_value_dev(h, flat0 + uint64_t(e));
+  }
+}
+
+__global__ void fill3d_kernel(Grid3D g, uint64_t h) {
+  const int64_t n = g.n, total = n * n * n;
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < total;
+       e += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t i = e / (n * n), rem = e - i * n * n, j = rem / n, k = rem - j * n;
+    g.origin[i * g.pitch_i + j * g.pitch_j + k] = init_value_dev(h, uint64_t(e));
+  }
+}
+
+__global__ void copy_rows_kernel(double* dst, int64_t ldd, const double* src, int64_t lds,
+                                 int64_t nrows, int64_t ncols, int64_t pd, int64_t rpp) {
+  const int64_t total = nrows * ncols;
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < total;
+       e += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t r = e / ncols, c = e - r * ncols;
+    const int64_t drow = rpp ? (r / rpp) * pd + (r % rpp) * ldd : r * ldd;
+    dst[drow + c] = src[r * lds + c];
+  }
+}
+
+__global__ void zero_ring2d_kernel(double* o, int64_t ld, int64_t n) {
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < 4 * n;
+       e += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t side = e / n, p = e - side * n;
+    int64_t r, c;
+    if (side == 0) r = 0, c = p;
+    else if (side == 1) r = n - 1, c = p;
+    else if (side == 2) r = p, c = 0;
+    else r = p, c = n - 1;
+    o[r * ld + c] = 0.0;
+  }
+}
+
+__global__ void zero_ring3d_kernel(Grid3D g) {
+  const int64_t n = g.n, total = n * n * n;
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < total;
+       e += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t i = e / (n * n), rem = e - i * n * n, j = rem / n, k = rem - j * n;
+    if (i == 0 || j == 0 || k == 0 || i == n - 1 || j == n - 1 || k == n - 1)
+      g.origin[i * g.pitch_i + j * g.pitch_j + k] = 0.0;
+  }
+}
+
+int grid_for(int64_t total) {
+  int64_t b = (total + 255) / 256;
+  if (b > 148 * 32) b = 148 * 32;
+  if (b < 1) b = 1;
+  return int(b);
+}
+
+}  // namespace
+
+uint64_t launches() { return g_launches.load(); }
+void count_launch(uint64_t n) { g_launches += n; }
+
+cudaError_t fill_init_value(double* dst, int64_t ld, int64_t nrows, int64_t ncols,
+                            uint64_t name_hash, uint64_t flat0, cudaStream_t stream) {
+  if (nrows <= 0 || ncols <= 0) return cudaSuccess;
+  fill2d_kernel<<<grid_for(nrows * ncols), 256, 0, stream>>>(dst, ld, nrows, ncols, name_hash,
+                                                             flat0);
+  count_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t fill_init_value_3d(const Grid3D& g, uint64_t name_hash, cudaStream_t stream) {
+  if (g.n <= 0) return cudaSuccess;
+  fill3d_kernel<<<grid_for(g.n * g.n * g.n), 256, 0, stream>>>(g, name_hash);
+  count_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t copy_rows(double* dst, int64_t ldd, const double* src, int64_t lds, int64_t nrows,
+                      int64_t ncols, cudaStream_t stream, int64_t pd, int64_t rpp) {
+  if (nrows <= 0 || ncols <= 0) return cudaSuccess;
+  copy_rows_kernel<<<grid_for(nrows * ncols), 256, 0, stream>>>(dst, ldd, src, lds, nrows, ncols,
+                                                                pd, rpp);
+  count_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t zero_ring_2d(double* origin, int64_t ld, int64_t n, cudaStream_t stream) {
+  if (n <= 0) return cudaSuccess;
+  zero_ring2d_kernel<<<grid_for(4 * n), 256, 0, stream>>>(origin, ld, n);
+  count_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t zero_ring_3d(const Grid3D& g, cudaStream_t stream) {
+  if (g.n <= 0) return cudaSuccess;
+  zero_ring3d_kernel<<<grid_for(g.n * g.n * g.n), 256, 0, stream>>>(g);
+  count_launch();
+  return cudaGetLastError();
+}
+
+}  // namespace pcotgpu

@@ -1,0 +1,190 @@
+"""Row-sharded 2-D 5-point stencil across ranks (one process per GPU).
+
+BASELINE config 4 / SURVEY.md §8(e): the grid's rows are split into
+contiguous slabs, one per rank; each slab carries `ghost` rows above and
+below.  One temporal block of depth bt reads the bt ghost rows on each side
+(the trapezoid shrinks by one row per step), so every bt steps each rank
+sends its first/last bt owned rows to its neighbours' ghost rows — the
+only data exchange.  The exchange is overlapped with compute: the boundary
+strips (rows [0, bt) and [R-bt, R)) are advanced first on one stream, their
+sends/recvs (torch.distributed, NCCL on GPUs) start as soon as they finish,
+and the interior rows are advanced concurrently on a second stream.
+
+The reference has no distributed path; results must equal the
+single-grid run bit for bit, which the per-point arithmetic guarantees as
+long as the ghost rows hold the neighbour's step-t0 values.
+
+The slab kernel is injected (`advance`) so the same exchange logic runs with
+the sm_100a kernel on GPUs and is tested with gloo on CPU.
+"""
+import ctypes
+
+import torch
+import torch.distributed as dist
+
+import paper_1802_00166_b200 as P
+
+
+def layout(rows, cols):
+    ld, ghost, padl, total = (ctypes.c_int64() for _ in range(4))
+    P._check(P.lib().pcotgpu_s2d5_layout(rows, cols, ctypes.byref(ld), ctypes.byref(ghost),
+                                         ctypes.byref(padl), ctypes.byref(total)))
+    return ld.value, ghost.value, padl.value, total.value
+
+
+class ShardedStencil2D:
+    """One rank's slab of an (R * world) x cols grid; ring rows/cols are the
+    global grid's edges (ring_hold=0: literal 0.0, 1: copied forward)."""
+
+    def __init__(self, rows_per_rank, cols, T, bt, ring_hold=0, order=0, device=None,
+                 advance=None, geometry=None, group=None):
+        self.rank = dist.get_rank() if dist.is_initialized() else 0
+        self.world = dist.get_world_size() if dist.is_initialized() else 1
+        self.group = group
+        self.R, self.cols, self.T, self.bt = int(rows_per_rank), int(cols), int(T), int(bt)
+        self.ring_hold, self.order = int(ring_hold), int(order)
+        self.g0 = self.rank * self.R
+        self.nrows = self.R * self.world
+        if self.R < 2 * self.bt and self.world > 1:
+            raise ValueError("slab must hold at least 2*bt rows")
+        self.device = device if device is not None else torch.device("cpu")
+        if geometry is None:
+            geometry = layout(self.R, self.cols)
+        self.ld, self.ghost, self.padl, total = geometry
+        if self.ghost < self.bt + 3:
+            raise ValueError("ghost rows < bt + 3")
+        self.buf = [torch.zeros(total, dtype=torch.float64, device=self.device) for _ in range(2)]
+        self.cur = 0
+        self.advance = advance or self._advance_cuda
+        self.on_gpu = self.device.type == "cuda"
+        if self.on_gpu:
+            self.s_edge = torch.cuda.Stream(device=self.device, priority=-1)
+            self.s_inner = torch.cuda.Stream(device=self.device)
+        self.kernel_events = []  # (start, end) CUDA events of every slab launch when timing
+
+    # -------------------------------------------------------------- views
+    def origin_offset(self):
+        return self.ghost * self.ld + self.padl
+
+    def rows_view(self, b, r0, r1):
+        """Flat contiguous view of local rows [r0, r1) (full pitch) of buffer b."""
+        base = (self.ghost + r0) * self.ld
+        return self.buf[b][base:base + (r1 - r0) * self.ld]
+
+    def interior(self, b):
+        """(R, cols) strided view of the owned cells of buffer b."""
+        v = self.buf[b][self.ghost * self.ld:(self.ghost + self.R) * self.ld].view(self.R, self.ld)
+        return v[:, self.padl:self.padl + self.cols]
+
+    def ptr(self, b):
+        return self.buf[b].data_ptr() + self.origin_offset() * 8
+
+    # -------------------------------------------------------------- init
+    def fill_init(self, name="F"):
+        """F[g, c] = init_value(name, g*cols + c) on owned rows, ring applied."""
+        b = self.cur
+        if self.on_gpu:
+            s = torch.cuda.current_stream(self.device)
+            P._check(P.lib().pcotgpu_fill_init_value(
+                ctypes.c_void_p(self.ptr(b)), self.ld, self.R, self.cols, name.encode(),
+                self.g0 * self.cols, ctypes.c_void_p(s.cuda_stream)))
+            P._check(P.lib().pcotgpu_s2d5_prepare(
+                ctypes.c_void_p(self.ptr(b)), self.R, self.cols, self.g0, self.nrows,
+                self.ring_hold, ctypes.c_void_p(s.cuda_stream)))
+        else:
+            raise RuntimeError("fill_init needs the GPU library; load values with load()")
+        self.exchange_sync(b)
+
+    def snapshot_input(self):
+        """Keep the step-0 slab (owned + ghost rows) so every run restarts from F,
+        as the reference's init statement re-reads F on every run."""
+        self.f0 = self.buf[self.cur].clone()
+
+    def restart(self):
+        self.buf[0].copy_(self.f0)
+        self.cur = 0
+
+    def load(self, values):
+        """Owned rows from a (R, cols) tensor (any device); ghosts from neighbours."""
+        self.interior(self.cur).copy_(values)
+        self.exchange_sync(self.cur)
+
+    # -------------------------------------------------------------- exchange
+    def _ops(self, b, depth):
+        ops = []
+        up, dn = self.rank - 1, self.rank + 1
+        g = self.group
+        if up >= 0:
+            ops.append(dist.P2POp(dist.isend, self.rows_view(b, 0, depth), up, g))
+            ops.append(dist.P2POp(dist.irecv, self.rows_view(b, -depth, 0), up, g))
+        if dn < self.world:
+            ops.append(dist.P2POp(dist.isend, self.rows_view(b, self.R - depth, self.R), dn, g))
+            ops.append(dist.P2POp(dist.irecv, self.rows_view(b, self.R, self.R + depth), dn, g))
+        return ops
+
+    def exchange_sync(self, b, depth=None):
+        if self.world == 1:
+            return
+        depth = depth or min(self.ghost, self.R)
+        ops = self._ops(b, depth)
+        for r in dist.batch_isend_irecv(ops):
+            r.wait()
+
+    # -------------------------------------------------------------- compute
+    def _advance_cuda(self, src, dst, row_lo, row_hi, bt, stream):
+        P._check(P.lib().pcotgpu_s2d5_advance(
+            ctypes.c_void_p(self.ptr(src)), ctypes.c_void_p(self.ptr(dst)), self.R, self.cols,
+            self.g0, self.nrows, bt, self.ring_hold, self.order, row_lo, row_hi,
+            ctypes.c_void_p(stream.cuda_stream if stream is not None else 0)))
+
+    def _timed(self, fn, stream, record):
+        if record and self.on_gpu:
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            fn()
+            e1.record(stream)
+            self.kernel_events.append((e0, e1))
+        else:
+            fn()
+
+    def block(self, bt, record=False):
+        """Advance all owned rows by bt steps, exchanging boundary rows."""
+        src, dst = self.cur, self.cur ^ 1
+        if self.world == 1:
+            stream = torch.cuda.current_stream(self.device) if self.on_gpu else None
+            self._timed(lambda: self.advance(src, dst, 0, self.R, bt, stream), stream, record)
+        elif not self.on_gpu:
+            self.advance(src, dst, 0, self.R, bt, None)
+            self.exchange_sync(dst, bt)
+        else:
+            main = torch.cuda.current_stream(self.device)
+            self.s_edge.wait_stream(main)
+            self.s_inner.wait_stream(main)
+            e = self.bt if self.R >= 2 * self.bt else self.R
+            with torch.cuda.stream(self.s_edge):
+                self._timed(lambda: self.advance(src, dst, 0, e, bt, self.s_edge), self.s_edge, record)
+                self._timed(lambda: self.advance(src, dst, self.R - e, self.R, bt, self.s_edge),
+                            self.s_edge, record)
+                reqs = dist.batch_isend_irecv(self._ops(dst, bt))
+            with torch.cuda.stream(self.s_inner):
+                self._timed(lambda: self.advance(src, dst, e, self.R - e, bt, self.s_inner),
+                            self.s_inner, record)
+            with torch.cuda.stream(self.s_edge):
+                for r in reqs:
+                    r.wait()
+            main.wait_stream(self.s_edge)
+            main.wait_stream(self.s_inner)
+        self.cur = dst
+
+    def run(self, record=False):
+        """T steps in blocks of bt (last block shorter)."""
+        t = 0
+        while t < self.T:
+            step = min(self.bt, self.T - t)
+            self.block(step, record)
+            t += step
+
+    def launches_per_run(self):
+        blocks = -(-self.T // self.bt)
+        return blocks * (1 if self.world == 1 else 3)
