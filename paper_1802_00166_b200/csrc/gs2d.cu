@@ -75,14 +75,13 @@ __global__ void gs2d_kernel(GsArgs g) {
     // region: i in [I0, I0+ni), s = i+j in [S0, S0+ns)
     const int64_t I0 = x0 - t0 - g.bt;
     const int64_t S0 = y0 - 2 * t0 - 2 * g.bt;
-    for (int r = tid / 32; r < g.ni; r += nthr / 32) {
+    for (int e = tid; e < g.ni * g.ns; e += nthr) {
+      const int r = e / g.ns, c = e - r * g.ns;
       const int64_t i = I0 + r;
-      for (int c = tid % 32; c < g.ns; c += 32) {
-        const int64_t j = S0 + c - i;
-        double v = 0.0;
-        if (i >= 0 && i < g.n && j >= 0 && j < g.n) v = ld_cg(g.a + i * g.ld + j);
-        reg[r * g.ns + c] = v;
-      }
+      const int64_t j = S0 + c - i;
+      double v = 0.0;
+      if (i >= 0 && i < g.n && j >= 0 && j < g.n) v = ld_cg(g.a + i * g.ld + j);
+      reg[e] = v;
     }
     __syncthreads();
     const int tt = tid / g.bx, xx = tid - (tid / g.bx) * g.bx;
