@@ -129,6 +129,10 @@ int pcotgpu_fill_init_value(double* dst, int64_t ld, int64_t nrows, int64_t ncol
 int pcotgpu_s2d5_prepare(double* origin, int64_t rows, int64_t cols, int64_t g0,
                          int64_t nrows_global, int ring_hold, void* stream);
 
+/* Test hook: q_fast[i] = the Gauss-Seidel kernel's x[i] / 9.0, q_ref[i] =
+ * IEEE __ddiv_rn(x[i], 9.0); device pointers. */
+int pcotgpu_test_div9(const double* x, double* q_fast, double* q_ref, int64_t n, void* stream);
+
 /* ---- misc ---------------------------------------------------------------- */
 const char* pcotgpu_last_error(void);
 uint64_t pcotgpu_launch_count(void);

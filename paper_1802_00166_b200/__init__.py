@@ -95,6 +95,8 @@ _SIGS = [
                                                ctypes.c_char_p, ctypes.c_uint64, ctypes.c_void_p]),
     ("pcotgpu_s2d5_prepare", ctypes.c_int, [ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64,
                                             ctypes.c_int64, ctypes.c_int, ctypes.c_void_p]),
+    ("pcotgpu_test_div9", ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64,
+                                         ctypes.c_void_p]),
     ("pcotgpu_last_error", ctypes.c_char_p, []),
     ("pcotgpu_launch_count", ctypes.c_uint64, []),
     ("pcotgpu_abi_version", ctypes.c_int, []),

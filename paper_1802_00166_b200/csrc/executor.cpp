@@ -43,7 +43,7 @@ int env_int(const char* name, int dflt) {
 
 constexpr int64_t kGhost = 16;  // ghost rows / halo planes (>= max bt + 3)
 constexpr int64_t kPadL = 16;   // left pad columns (128 B)
-constexpr int64_t kPadR2 = 528; // right pad for the 2-D strip window (>= W_IN + 2 + pad)
+constexpr int64_t kPadR2 = 1040; // right pad for the 2-D strip window (>= W_IN + 2, widest variant)
 constexpr int64_t kPadR3 = 80;  // right pad for the 3-D window (>= 66 + halo)
 
 struct DevBuf {
@@ -632,6 +632,10 @@ int pcotgpu_s2d5_advance(const double* in_origin, double* out_origin, int64_t ro
   a.padl = b.padl = kPadL;
   return cuda_status(s2d5_advance(a, b, g0, nrows_global, bt, ring_hold, order, int(row_lo),
                                   int(row_hi), static_cast<cudaStream_t>(stream)));
+}
+
+int pcotgpu_test_div9(const double* x, double* q_fast, double* q_ref, int64_t n, void* stream) {
+  return cuda_status(div9_check(x, q_fast, q_ref, n, static_cast<cudaStream_t>(stream)));
 }
 
 int pcotgpu_fill_init_value(double* dst, int64_t ld, int64_t nrows, int64_t ncols, const char* name,

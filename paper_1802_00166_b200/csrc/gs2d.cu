@@ -40,6 +40,27 @@ struct GsPlan {
 
 namespace {
 
+// Correctly rounded x / 9.0 without the general division sequence:
+// q0 = RN(x * RN(1/9)) is within 1 ulp of x/9, so r = x - 9*q0 is exact
+// (one FMA) and RN(q0 + r * RN(1/9)) is the correctly rounded quotient
+// (Markstein's correction theorem for a divisor known in advance).  Verified
+// against __ddiv_rn on the device (tests/test_gpu_kernels.py) and through the
+// Gauss-Seidel goldens.
+PCOT_DEV double div9(double x) {
+  const double y = 0.1111111111111111049432054187491303309798240661621094;  // RN(1/9)
+  const double q0 = __dmul_rn(x, y);
+  const double r = __fma_rn(-q0, 9.0, x);
+  return __fma_rn(r, y, q0);
+}
+
+__global__ void div9_check_kernel(const double* x, double* q_fast, double* q_ref, int64_t n) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    q_fast[i] = div9(x[i]);
+    q_ref[i] = __ddiv_rn(x[i], 9.0);
+  }
+}
+
 struct GsArgs {
   double* a;
   int64_t ld, n, T;
@@ -108,7 +129,7 @@ __global__ void gs2d_kernel(GsArgs g) {
           acc = add(acc, dn[0]);
           acc = add(acc, dn[1]);
           acc = add(acc, dn[2]);
-          const double v = div(acc, 9.0);
+          const double v = div9(acc);
           me[0] = v;
           g.a[i * g.ld + j] = v;
         }
@@ -194,6 +215,13 @@ void gs2d_plan_destroy(GsPlan* p) {
 }
 
 int64_t gs2d_plan_tiles(const GsPlan* p) { return p ? p->ntiles : 0; }
+
+cudaError_t div9_check(const double* x, double* q_fast, double* q_ref, int64_t n,
+                       cudaStream_t stream) {
+  div9_check_kernel<<<148 * 8, 256, 0, stream>>>(x, q_fast, q_ref, n);
+  count_launch();
+  return cudaGetLastError();
+}
 
 cudaError_t gs2d_run(GsPlan* p, double* a, int64_t ld, cudaStream_t stream) {
   if (p->ntiles == 0) return cudaSuccess;

@@ -49,6 +49,9 @@ GsPlan* gs2d_plan_create(int64_t n, int64_t T, int bt, int bx, int by, int devic
 void gs2d_plan_destroy(GsPlan* p);
 cudaError_t gs2d_run(GsPlan* p, double* a, int64_t ld, cudaStream_t stream);
 int64_t gs2d_plan_tiles(const GsPlan* p);
+// Test hook: the Gauss-Seidel kernel's x/9 vs the IEEE division, elementwise.
+cudaError_t div9_check(const double* x, double* q_fast, double* q_ref, int64_t n,
+                       cudaStream_t stream);
 
 // C = A*B, fp64 DMMA tensor cores, row-major N x N with pitch ld.
 cudaError_t dgemm_nn(const double* A, const double* B, double* C, int64_t n, int64_t ld,

@@ -3,7 +3,7 @@
 // Replaces the reference's interpreted hot loop for heat2d/jacobi2d
 // (reference core/src/exec.cpp:347-428 exec_stmt over kernels/heat2d.kernel:32)
 // and the tile order that feeds it (tiler.cpp:189-243): one launch advances the
-// grid `BT` time steps per HBM round trip.
+// grid `BT` time steps per HBM round trip (16/BT algorithmic bytes per update).
 //
 // Tile = column strip (W_IN = NT*C input columns, W_OUT = W_IN - 2*BT output
 // columns) x row chunk [r0, r1).  The CTA streams input rows r0-BT .. r1+BT-1:
@@ -13,11 +13,13 @@
 //     three rows in registers (slot = row mod 3, loop unrolled by 3 so every
 //     register index is static);
 //   * level L+1 row rho needs level L rows rho-1..rho+1 of its own columns
-//     (registers) and the west/east neighbours at row rho: warp shuffles
-//     inside a warp, a double-buffered shared-memory edge exchange across
-//     warps (one __syncthreads per input row).
+//     (registers) and the west/east neighbours at row rho, produced one
+//     iteration earlier: warp shuffles inside a warp, a double-buffered
+//     shared-memory edge exchange across warps (one __syncthreads per row).
 // Operation order per point is the reference body's parse tree:
 //   0.2 * ((((c + (i-1,j)) + (i+1,j)) + (i,j-1)) + (i,j+1)), no FMA.
+#include <cstdlib>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -25,30 +27,25 @@ namespace pcotgpu {
 
 namespace {
 
-constexpr int kC = 2;      // columns per thread
-constexpr int kNT = 256;   // threads per CTA
-constexpr int kPF = 8;     // TMA ring depth (rows in flight)
+constexpr int kPF = 8;  // TMA ring depth (rows in flight)
 
 struct S2Args {
   const double* in;
   double* out;
   int64_t ld_in, ld_out;
-  int64_t cols;      // N
-  int64_t g0;        // global row of local row 0
-  int64_t nrows;     // global rows
-  int64_t row_lo, row_hi;  // local rows produced
+  int64_t cols;              // N
+  int64_t g0;                // global row of local row 0
+  int64_t nrows;             // global rows
+  int64_t row_lo, row_hi;    // local rows produced
   int64_t load_lo, load_hi;  // clamp range for input rows
-  int H;             // chunk height
+  int H;                     // chunk height
   int nstrips, nchunks;
   int order;
   int w_out;
 };
 
-PCOT_DEV int pmod3(int v) { return ((v % 3) + 3) % 3; }
-
-// Morton (Z-order) decode of a linear tile id over a 2^k x 2^k covering grid
-// (COT-style recursive order, reference tiler.cpp:150-203); ids landing outside
-// the real grid are skipped by the caller via the returned flag.
+// Tile id -> (strip, chunk): lexicographic (SLT-like) or Morton/Z order over a
+// power-of-two cover (the COT recursive order, reference tiler.cpp:150-203).
 PCOT_DEV bool tile_coords(int id, int nstrips, int nchunks, int order, int& strip, int& chunk) {
   if (order == kOrderLex) {
     chunk = id / nstrips;
@@ -65,43 +62,58 @@ PCOT_DEV bool tile_coords(int id, int nstrips, int nchunks, int order, int& stri
   return strip < nstrips && chunk < nchunks;
 }
 
-template <int BT>
+__host__ __device__ constexpr int smod3(int v) { return ((v % 3) + 3) % 3; }
+
+template <int BT, int C>
 struct Regs {
-  double v[BT][3][kC];
+  double v[BT][3][C];
 };
 
-template <int BT, bool MASK, bool HOLD, int P>
-PCOT_DEV void s2d5_iter(Regs<BT>& R, const double* __restrict__ ring_row, int shift, int64_t k,
-                        int par, double* __restrict__ edge, int warp, int lane,
-                        int nwarps, const S2Args& a, int64_t cb, int64_t r0, int64_t r1,
-                        int64_t c0, int64_t cend) {
+template <int BT, int C, int NT, bool MASK, bool HOLD, int P>
+PCOT_DEV void s2d5_iter(Regs<BT, C>& R, const double* __restrict__ ring_row, int64_t k, int par,
+                        double* __restrict__ edge, int warp, int lane, const S2Args& a,
+                        int64_t cb, int64_t r0, int64_t r1, int64_t c0, int64_t cend,
+                        bool full_cols) {
+  constexpr int NW = NT / 32;
+  constexpr int SHIFT = BT & 1;  // (c0 - BT) - even load start
   // ---- level 0: input row k
   {
-    constexpr int s = ((P % 3) + 3) % 3;
-    const double* src = ring_row + shift + threadIdx.x * kC;
+    constexpr int s = smod3(P);
+    const double* src = ring_row + SHIFT + threadIdx.x * C;
+    if constexpr (SHIFT == 0 && C % 2 == 0) {
 #pragma unroll
-    for (int c = 0; c < kC; ++c) R.v[0][s][c] = src[c];
+      for (int c = 0; c < C; c += 2) {
+        const double2 v = *reinterpret_cast<const double2*>(src + c);
+        R.v[0][s][c] = v.x;
+        R.v[0][s][c + 1] = v.y;
+      }
+    } else {
+#pragma unroll
+      for (int c = 0; c < C; ++c) R.v[0][s][c] = src[c];
+    }
   }
-  const double* eprev = edge + (par ^ 1) * (nwarps * 2 * BT);  // written at k-1
+  const double* eprev = edge + (par ^ 1) * (NW * 2 * BT);  // written at k-1
+  double* ecur = edge + par * (NW * 2 * BT);
 #pragma unroll
   for (int L = 0; L < BT; ++L) {
-    const int rho_rel = P - L - 1;  // (rho - kstart) mod 3 basis, static
-    const int sm = ((rho_rel % 3) + 3) % 3;
-    const int st = (((rho_rel - 1) % 3) + 3) % 3;
-    const int sb = (((rho_rel + 1) % 3) + 3) % 3;
+    constexpr int dummy = 0;
+    (void)dummy;
+    const int sm = smod3(P - L - 1);
+    const int st = smod3(P - L - 2);
+    const int sb = smod3(P - L);
     const double* top = R.v[L][st];
     const double* mid = R.v[L][sm];
     const double* bot = R.v[L][sb];
-    double W = __shfl_up_sync(0xffffffffu, mid[kC - 1], 1);
+    double W = __shfl_up_sync(0xffffffffu, mid[C - 1], 1);
     double E = __shfl_down_sync(0xffffffffu, mid[0], 1);
     if (lane == 0 && warp > 0) W = eprev[((warp - 1) * 2 + 1) * BT + L];
-    if (lane == 31 && warp + 1 < nwarps) E = eprev[((warp + 1) * 2 + 0) * BT + L];
+    if (lane == 31 && warp + 1 < NW) E = eprev[((warp + 1) * 2 + 0) * BT + L];
     const int64_t rho = k - L - 1;
-    double nv[kC];
+    double nv[C];
 #pragma unroll
-    for (int c = 0; c < kC; ++c) {
-      double left = c > 0 ? mid[c - 1] : W;
-      double right = c < kC - 1 ? mid[c + 1] : E;
+    for (int c = 0; c < C; ++c) {
+      const double left = c > 0 ? mid[c > 0 ? c - 1 : 0] : W;
+      const double right = c < C - 1 ? mid[c < C - 1 ? c + 1 : 0] : E;
       double s = add(mid[c], top[c]);
       s = add(s, bot[c]);
       s = add(s, left);
@@ -112,7 +124,7 @@ PCOT_DEV void s2d5_iter(Regs<BT>& R, const double* __restrict__ ring_row, int sh
       const int64_t gr = a.g0 + rho;
       const bool row_in = gr >= 1 && gr <= a.nrows - 2;
 #pragma unroll
-      for (int c = 0; c < kC; ++c) {
+      for (int c = 0; c < C; ++c) {
         const int64_t col = cb + c;
         const bool in = row_in && col >= 1 && col <= a.cols - 2;
         if (!in) nv[c] = HOLD ? mid[c] : 0.0;
@@ -120,43 +132,38 @@ PCOT_DEV void s2d5_iter(Regs<BT>& R, const double* __restrict__ ring_row, int sh
     }
     if (L + 1 < BT) {
 #pragma unroll
-      for (int c = 0; c < kC; ++c) R.v[(L + 1) < BT ? L + 1 : 0][sm][c] = nv[c];
-    } else {
-      if (rho >= r0 && rho < r1) {
-        double* dst = a.out + rho * a.ld_out;
+      for (int c = 0; c < C; ++c) R.v[L + 1 < BT ? L + 1 : 0][sm][c] = nv[c];
+    } else if (rho >= r0 && rho < r1) {
+      double* dst = a.out + rho * a.ld_out + cb;
+      if (SHIFT == 0 && C % 2 == 0 && full_cols) {
 #pragma unroll
-        for (int c = 0; c < kC; ++c) {
+        for (int c = 0; c < C; c += 2)
+          __stcs(reinterpret_cast<double2*>(dst + c), make_double2(nv[c], nv[c + 1]));
+      } else {
+#pragma unroll
+        for (int c = 0; c < C; ++c) {
           const int64_t col = cb + c;
-          if (col >= c0 && col < cend) __stcs(dst + col, nv[c]);
+          if (col >= c0 && col < cend) __stcs(dst + c, nv[c]);
         }
       }
     }
   }
   // ---- publish this iteration's newest row edges of every level (rows k-L)
-  double* ecur = edge + par * (nwarps * 2 * BT);
   if (lane == 0) {
 #pragma unroll
-    for (int L = 0; L < BT; ++L) {
-      const int s = (((P - L) % 3) + 3) % 3;
-      ecur[(warp * 2 + 0) * BT + L] = R.v[L][s][0];
-    }
+    for (int L = 0; L < BT; ++L) ecur[(warp * 2 + 0) * BT + L] = R.v[L][smod3(P - L)][0];
   }
   if (lane == 31) {
 #pragma unroll
-    for (int L = 0; L < BT; ++L) {
-      const int s = (((P - L) % 3) + 3) % 3;
-      ecur[(warp * 2 + 1) * BT + L] = R.v[L][s][kC - 1];
-    }
+    for (int L = 0; L < BT; ++L) ecur[(warp * 2 + 1) * BT + L] = R.v[L][smod3(P - L)][C - 1];
   }
 }
 
-template <int BT, bool MASK, bool HOLD>
+template <int BT, int C, int NT, bool MASK, bool HOLD>
 PCOT_DEV void s2d5_tile(const S2Args& a, int strip, int chunk, double* ring, uint64_t* bars,
                         double* edge) {
-  constexpr int W_IN = kNT * kC;
-  constexpr int W_LOAD = W_IN + 2;
+  constexpr int W_LOAD = NT * C + 2;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  constexpr int nwarps = kNT / 32;
   const int64_t c0 = int64_t(strip) * a.w_out;
   const int64_t cend = c0 + a.w_out < a.cols ? c0 + a.w_out : a.cols;
   const int64_t r0 = a.row_lo + int64_t(chunk) * a.H;
@@ -164,9 +171,9 @@ PCOT_DEV void s2d5_tile(const S2Args& a, int strip, int chunk, double* ring, uin
   const int64_t kstart = r0 - BT;
   const int64_t niter = ((r1 + BT - kstart) + 2) / 3 * 3;
   const int64_t cfirst = c0 - BT;
-  const int64_t cs = cfirst >= 0 ? (cfirst & ~int64_t(1)) : -((-cfirst + 1) & ~int64_t(1));
-  const int shift = int(cfirst - cs);
-  const int64_t cb = cfirst + tid * kC;
+  const int64_t cs = cfirst - (BT & 1);  // even: 16-B aligned bulk copy source
+  const int64_t cb = cfirst + tid * C;
+  const bool full_cols = cb >= c0 && cb + C <= cend;
 
   auto issue = [&](int64_t it) {
     int64_t row = kstart + it;
@@ -178,24 +185,27 @@ PCOT_DEV void s2d5_tile(const S2Args& a, int strip, int chunk, double* ring, uin
   if (tid == 0) {
     for (int it = 0; it < kPF && it < niter; ++it) issue(it);
   }
-  Regs<BT> R;
+  Regs<BT, C> R;
 #pragma unroll
   for (int L = 0; L < BT; ++L)
 #pragma unroll
     for (int s = 0; s < 3; ++s)
 #pragma unroll
-      for (int c = 0; c < kC; ++c) R.v[L][s][c] = 0.0;
+      for (int c = 0; c < C; ++c) R.v[L][s][c] = 0.0;
 
+  // Every warp waits on the row's mbarrier itself (measured faster than one
+  // waiter + the barrier: the try_wait latency then overlaps across warps).
   for (int64_t it = 0; it < niter; it += 3) {
-#define PCOT_S2_STEP(P)                                                                    \
-  {                                                                                        \
-    const int64_t itp = it + P;                                                            \
-    const int slot = int(itp % kPF);                                                       \
-    mbar_wait(&bars[slot], uint32_t((itp / kPF) & 1));                                     \
-    s2d5_iter<BT, MASK, HOLD, P>(R, ring + slot * W_LOAD, shift, kstart + itp, int(itp & 1),  \
-                                 edge, warp, lane, nwarps, a, cb, r0, r1, c0, cend);        \
-    __syncthreads();                                                                       \
-    if (tid == 0 && itp + kPF < niter) issue(itp + kPF);                                   \
+#define PCOT_S2_STEP(P)                                                                      \
+  {                                                                                          \
+    const int64_t itp = it + P;                                                              \
+    const int slot = int(itp % kPF);                                                         \
+    mbar_wait(&bars[slot], uint32_t((itp / kPF) & 1));                                       \
+    s2d5_iter<BT, C, NT, MASK, HOLD, P>(R, ring + slot * W_LOAD, kstart + itp, int(itp & 1), \
+                                        edge, warp, lane, a, cb, r0, r1, c0, cend,            \
+                                        full_cols);                                          \
+    __syncthreads();                                                                         \
+    if (tid == 0 && itp + kPF < niter) issue(itp + kPF);                                     \
   }
     PCOT_S2_STEP(0)
     PCOT_S2_STEP(1)
@@ -204,12 +214,13 @@ PCOT_DEV void s2d5_tile(const S2Args& a, int strip, int chunk, double* ring, uin
   }
 }
 
-template <int BT, bool HOLD>
-__global__ void __launch_bounds__(kNT, 2) s2d5_kernel(S2Args a) {
-  constexpr int W_LOAD = kNT * kC + 2;
-  __shared__ __align__(128) double ring[kPF * W_LOAD];
-  __shared__ __align__(16) double edge[2 * (kNT / 32) * 2 * BT];
-  __shared__ __align__(8) uint64_t bars[kPF];
+template <int BT, int C, int NT, int MINB, bool HOLD>
+__global__ void __launch_bounds__(NT, MINB) s2d5_kernel(S2Args a) {
+  constexpr int W_LOAD = NT * C + 2;
+  extern __shared__ __align__(128) double smem2[];
+  double* ring = smem2;
+  double* edge = ring + kPF * W_LOAD;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(edge + 2 * (NT / 32) * 2 * BT);
   int strip, chunk;
   if (!tile_coords(blockIdx.x, a.nstrips, a.nchunks, a.order, strip, chunk)) return;
   if (threadIdx.x == 0) {
@@ -220,18 +231,52 @@ __global__ void __launch_bounds__(kNT, 2) s2d5_kernel(S2Args a) {
   const int64_t c0 = int64_t(strip) * a.w_out;
   const int64_t r0 = a.row_lo + int64_t(chunk) * a.H;
   const int64_t r1 = r0 + a.H < a.row_hi ? r0 + a.H : a.row_hi;
-  // Cells whose update can hit the ring (or the outside) need the masked body.
+  // Tiles whose dependence cone touches the ring (or the outside) need the masked body.
   const bool edge_tile = (c0 - BT <= 0) || (c0 + a.w_out + BT >= a.cols - 1) ||
                          (a.g0 + r0 - BT <= 0) || (a.g0 + r1 + BT >= a.nrows - 1);
   if (edge_tile)
-    s2d5_tile<BT, true, HOLD>(a, strip, chunk, ring, bars, edge);
+    s2d5_tile<BT, C, NT, true, HOLD>(a, strip, chunk, ring, bars, edge);
   else
-    s2d5_tile<BT, false, HOLD>(a, strip, chunk, ring, bars, edge);
+    s2d5_tile<BT, C, NT, false, HOLD>(a, strip, chunk, ring, bars, edge);
 }
 
-template <int BT>
-cudaError_t launch_bt(const S2Args& a0, int ring_hold, cudaStream_t stream) {
-  S2Args a = a0;
+// Pick the chunk height so the grid fills whole waves of resident CTAs:
+// minimise waves * (H + 2*BT + 2) (time ~ rounds x rows streamed per tile).
+void size_grid(S2Args& a, int bt, int rows, int slots) {
+  const int hmin = 16 * bt > 48 ? 16 * bt : 48;
+  int best_n = 1;
+  double best = 1e300;
+  const int maxc = rows / hmin > 1 ? rows / hmin : 1;
+  for (int nc = 1; nc <= maxc; ++nc) {
+    const int H = (rows + nc - 1) / nc;
+    const int64_t tiles = int64_t(a.nstrips) * nc;
+    const int64_t waves = (tiles + slots - 1) / slots;
+    const double cost = double(waves) * (H + 2 * bt + 2);
+    if (cost < best * 0.999) best = cost, best_n = nc;
+  }
+  a.nchunks = best_n;
+  a.H = (rows + best_n - 1) / best_n;
+}
+
+template <int BT, int C, int NT, int MINB>
+cudaError_t launch_cfg(S2Args a, int ring_hold, int rows, cudaStream_t stream) {
+  auto kern = ring_hold ? s2d5_kernel<BT, C, NT, MINB, true> : s2d5_kernel<BT, C, NT, MINB, false>;
+  constexpr size_t smem = size_t(kPF) * (NT * C + 2) * 8 + size_t(2) * (NT / 32) * 2 * BT * 8 +
+                          size_t(kPF) * 8;
+  static int slots[2] = {0, 0};
+  int& sl = slots[ring_hold ? 1 : 0];
+  if (sl == 0) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    if (e != cudaSuccess) return e;
+    int occ = 0, sms = 0, dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, NT, smem);
+    sl = (occ > 0 ? occ : 1) * (sms > 0 ? sms : 148);
+  }
+  a.w_out = NT * C - 2 * BT;
+  a.nstrips = int((a.cols + a.w_out - 1) / a.w_out);
+  size_grid(a, BT, rows, sl);
   int grid;
   if (a.order == kOrderMorton) {
     int side = 1;
@@ -240,17 +285,30 @@ cudaError_t launch_bt(const S2Args& a0, int ring_hold, cudaStream_t stream) {
   } else {
     grid = a.nstrips * a.nchunks;
   }
-  if (ring_hold)
-    s2d5_kernel<BT, true><<<grid, kNT, 0, stream>>>(a);
-  else
-    s2d5_kernel<BT, false><<<grid, kNT, 0, stream>>>(a);
+  kern<<<grid, NT, smem, stream>>>(a);
   count_launch();
   return cudaGetLastError();
+}
+
+// Variant table: (C, NT, MINB).  Variant 0 is the default; PCOTGPU_S2D5_VARIANT
+// selects another for tuning.
+template <int BT>
+cudaError_t launch_bt(const S2Args& a, int ring_hold, int rows, int variant, cudaStream_t s) {
+  if (variant < 0)  // measured best per depth (tools/kbench.py s2d5; profiles/)
+    variant = (BT == 5 || BT == 6) && !ring_hold ? 3 : 0;
+  switch (variant) {
+    case 1: return launch_cfg<BT, 2, 256, 2>(a, ring_hold, rows, s);
+    case 2: return launch_cfg<BT, 4, 256, 1>(a, ring_hold, rows, s);
+    case 3: return launch_cfg<BT, 4, 128, 3>(a, ring_hold, rows, s);
+    default: return launch_cfg<BT, 4, 128, 2>(a, ring_hold, rows, s);
+  }
 }
 
 }  // namespace
 
 int s2d5_max_bt() { return 8; }
+
+int s2d5_window_cols() { return 1024 + 2; }
 
 cudaError_t s2d5_advance(const Slab2D& in, const Slab2D& out, int64_t g0, int64_t nrows,
                          int bt, int ring_hold, int order, int row_lo, int row_hi,
@@ -271,27 +329,22 @@ cudaError_t s2d5_advance(const Slab2D& in, const Slab2D& out, int64_t g0, int64_
   a.row_hi = row_hi;
   a.load_lo = -in.ghost;
   a.load_hi = in.rows + in.ghost - 1;
-  a.w_out = kNT * kC - 2 * bt;
-  a.nstrips = int((in.cols + a.w_out - 1) / a.w_out);
-  // Enough CTAs for ~8 per SM, chunks no shorter than 16*BT rows.
-  const int64_t rows = row_hi - row_lo;
-  int64_t want = (148 * 8 + a.nstrips - 1) / a.nstrips;
-  int64_t H = (rows + want - 1) / want;
-  if (H < 16 * bt) H = 16 * bt;
-  if (H > rows) H = rows;
-  a.H = int(H);
-  a.nchunks = int((rows + H - 1) / H);
   a.order = order;
-  // right padding must cover the last strip's W_IN+2 load window
+  static int variant = -2;
+  if (variant == -2) {
+    const char* v = std::getenv("PCOTGPU_S2D5_VARIANT");
+    variant = v ? std::atoi(v) : -1;  // -1: automatic per depth
+  }
+  const int rows = row_hi - row_lo;
   switch (bt) {
-    case 1: return launch_bt<1>(a, ring_hold, stream);
-    case 2: return launch_bt<2>(a, ring_hold, stream);
-    case 3: return launch_bt<3>(a, ring_hold, stream);
-    case 4: return launch_bt<4>(a, ring_hold, stream);
-    case 5: return launch_bt<5>(a, ring_hold, stream);
-    case 6: return launch_bt<6>(a, ring_hold, stream);
-    case 7: return launch_bt<7>(a, ring_hold, stream);
-    default: return launch_bt<8>(a, ring_hold, stream);
+    case 1: return launch_bt<1>(a, ring_hold, rows, variant, stream);
+    case 2: return launch_bt<2>(a, ring_hold, rows, variant, stream);
+    case 3: return launch_bt<3>(a, ring_hold, rows, variant, stream);
+    case 4: return launch_bt<4>(a, ring_hold, rows, variant, stream);
+    case 5: return launch_bt<5>(a, ring_hold, rows, variant, stream);
+    case 6: return launch_bt<6>(a, ring_hold, rows, variant, stream);
+    case 7: return launch_bt<7>(a, ring_hold, rows, variant, stream);
+    default: return launch_bt<8>(a, ring_hold, rows, variant, stream);
   }
 }
 

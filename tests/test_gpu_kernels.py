@@ -1,0 +1,90 @@
+"""GPU: kernel-level properties that the end-to-end goldens do not isolate."""
+import ctypes
+
+import numpy as np
+import pytest
+
+import paper_1802_00166_b200 as P
+from tests import oracle_ctypes as O
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+def test_gauss_seidel_division_is_ieee_correctly_rounded():
+    """The Gauss-Seidel kernel divides by 9.0 with a Markstein correction
+    instead of the general division; it must equal __ddiv_rn bit for bit."""
+    n = 1 << 26
+    g = torch.Generator(device="cuda").manual_seed(1234)
+    xs = [torch.rand(n, dtype=torch.float64, device="cuda", generator=g) * 9.0,
+          torch.rand(n, dtype=torch.float64, device="cuda", generator=g),
+          # sums of 9 cells of [0,1) values and their ulp neighbourhoods
+          torch.rand(n, dtype=torch.float64, device="cuda", generator=g) * 9.0 + 1e-300]
+    specials = torch.tensor([0.0, 9.0, 1.0, 4.5, 8.999999999999998, 2.0 ** -1000, 1e-310, 3.0,
+                             27.0, 81.0, 6.0, 0.1111111111111111], dtype=torch.float64, device="cuda")
+    ints = torch.arange(0, 1 << 20, dtype=torch.float64, device="cuda")
+    # exact multiples of 9 and near-midpoint quotients
+    mult = ints * 9.0
+    bits = torch.randint(0, 1 << 52, (n,), generator=g, device="cuda", dtype=torch.int64)
+    dense = (bits | (1023 << 52)).view(torch.float64) * 8.0  # [8, 16): every mantissa pattern
+    for x in xs + [specials, ints, mult, dense]:
+        q = torch.empty_like(x)
+        r = torch.empty_like(x)
+        s = torch.cuda.current_stream().cuda_stream
+        P._check(P.lib().pcotgpu_test_div9(ctypes.c_void_p(x.data_ptr()), ctypes.c_void_p(q.data_ptr()),
+                                           ctypes.c_void_p(r.data_ptr()), x.numel(), ctypes.c_void_p(s)))
+        torch.cuda.synchronize()
+        assert torch.equal(q.view(torch.int64), r.view(torch.int64))
+
+
+def test_sharded_slabs_equal_single_grid_on_one_gpu():
+    """The row-sharded driver's slab kernel on sub-ranges of rows (as the
+    multi-GPU path launches it: boundary strips + interior) reproduces the
+    single-launch result bit for bit."""
+    from paper_1802_00166_b200.sharded import ShardedStencil2D
+
+    N, T, bt = 1000, 40, 6
+    dev = torch.device("cuda", 0)
+    S = ShardedStencil2D(N, N, T, bt, device=dev)
+    S.fill_init("F")
+    S.snapshot_input()
+    S.run()
+    full = S.interior(S.cur).cpu().numpy().copy()
+    want = O.reference_output("jacobi2d", {"T": T, "N": N}).reshape(N, N)
+    assert np.array_equal(full.view(np.uint64), want.view(np.uint64))
+    # same run, every block split into three launches over row ranges
+    S.restart()
+    t = 0
+    while t < T:
+        step = min(bt, T - t)
+        src, dst = S.cur, S.cur ^ 1
+        stream = torch.cuda.current_stream()
+        for lo, hi in [(0, step), (N - step, N), (step, N - step)]:
+            S.advance(src, dst, lo, hi, step, stream)
+        S.cur = dst
+        t += step
+    split = S.interior(S.cur).cpu().numpy()
+    assert np.array_equal(split.view(np.uint64), want.view(np.uint64))
+
+
+@pytest.mark.parametrize("variant", [0, 1, 2, 3])
+def test_s2d5_variants_bit_exact(variant, monkeypatch):
+    """Every compiled (C, NT, MINB) variant of the 2-D kernel, all depths."""
+    import subprocess
+    import sys
+
+    code = (
+        "import numpy as np, paper_1802_00166_b200 as P\n"
+        "from tests import oracle_ctypes as O\n"
+        "want = O.reference_output('jacobi2d', {'T': 24, 'N': 777})\n"
+        "with P.GpuExecutor('jacobi2d', {'T': 24, 'N': 777}) as ex:\n"
+        "    for bt in range(1, 9):\n"
+        "        ex.run('slt', [bt, 8, 8], skip_checksum=True)\n"
+        "        out = ex.array_data('Out')\n"
+        "        assert np.array_equal(out.view(np.uint64), want.view(np.uint64)), bt\n"
+        "print('ok')\n")
+    env = dict(**__import__("os").environ, PCOTGPU_S2D5_VARIANT=str(variant))
+    p = subprocess.run([sys.executable, "-c", code], cwd=O.REPO, env=env, capture_output=True,
+                       text=True, timeout=600)
+    assert p.returncode == 0 and "ok" in p.stdout, p.stdout + p.stderr

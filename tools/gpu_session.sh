@@ -1,8 +1,6 @@
 cd $GRAFT_REPO_ROOT
-./tools/fp64_peaks > gpurun_out/fp64_peaks.log 2>&1
-timeout 300 python tools/kbench.py s2d5 > gpurun_out/kb_s2d5.log 2>&1
-timeout 300 python tools/kbench.py s3d7 --bts 1,2,3,4 > gpurun_out/kb_s3d7.log 2>&1
-timeout 300 python tools/kbench.py gs --tiles 4x32x256,8x32x256,4x64x256,8x64x128,2x32x512 > gpurun_out/kb_gs.log 2>&1
-timeout 300 python tools/kbench.py gemm > gpurun_out/kb_gemm.log 2>&1
-timeout 1200 python -m pytest tests/test_gpu_parity.py -q -m gpu -k "gs2d or gemm or storage or host or config4" > gpurun_out/pytest_gpu2.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu2.log
-cat gpurun_out/fp64_peaks.log gpurun_out/kb_*.log; tail -15 gpurun_out/pytest_gpu2.log
+timeout 900 python -m pytest tests/test_gpu_kernels.py tests/test_gpu_parity.py -q -m gpu -x > gpurun_out/pytest_gpu3.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu3.log
+for v in 0 3; do echo "variant $v"; PCOTGPU_S2D5_VARIANT=$v timeout 300 python tools/kbench.py s2d5 --bts 4,5,6,7,8 --orders slt 2>&1 | grep -v Warn; done > gpurun_out/kb_variants2.log 2>&1
+timeout 300 python tools/kbench.py gs --tiles 8x64x128,16x64x128,8x128x64,16x32x256,4x128x128,32x32x128 > gpurun_out/kb_gs2.log 2>&1
+timeout 600 python bench.py --steps 3 --warmup 2 > gpurun_out/bench2.log 2>&1; echo "bench rc=$?" >> gpurun_out/bench2.log
+tail -4 gpurun_out/pytest_gpu3.log; cat gpurun_out/kb_variants2.log gpurun_out/kb_gs2.log; tail -2 gpurun_out/bench2.log

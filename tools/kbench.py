@@ -38,8 +38,9 @@ def s2d5(a):
     S = ShardedStencil2D(a.rows, a.cols, 8, 8, device=torch.device("cuda", 0))
     S.fill_init("F")
     cells = a.rows * a.cols
+    orders = [0] if a.orders == "slt" else [1] if a.orders == "cot" else [0, 1]
     for bt in [int(x) for x in a.bts.split(",")]:
-        for order in (0, 1):
+        for order in orders:
             S.order = order
 
             def one():
@@ -71,6 +72,7 @@ def main():
     ap.add_argument("--T", type=int, default=0)
     ap.add_argument("--tiles", default="")
     ap.add_argument("--reps", type=int, default=3)
+    ap.add_argument("--orders", default="both")
     a = ap.parse_args()
     torch.cuda.set_device(0)
     if a.which == "s2d5":
