@@ -69,17 +69,33 @@ struct Regs {
   double v[BT][3][C];
 };
 
-template <int BT, int C, int NT, bool MASK, bool HOLD, int P>
-PCOT_DEV void s2d5_iter(Regs<BT, C>& R, const double* __restrict__ ring_row, int64_t k, int par,
+// Edge exchange: XS = false -> warp shuffles + smem only across warps;
+// XS = true -> every thread publishes its first/last column of every level's
+// newest row in shared memory (2 STS) and reads its neighbours' (2 LDS): no
+// shuffles, no selects, no predicates (measured: fewer instructions/update).
+template <int BT, int NT, bool XS>
+struct EdgeLayout {
+  static constexpr int kPerPar = XS ? BT * 2 * (NT + 2) : (NT / 32) * 2 * BT;
+  static constexpr int kDoubles = 2 * kPerPar;
+};
+
+template <int BT, int C, int NT, bool MASK, bool HOLD, bool XS, int P>
+PCOT_DEV void s2d5_iter(Regs<BT, C>& R, const double* __restrict__ ring_row, int k, int par,
                         double* __restrict__ edge, int warp, int lane, const S2Args& a,
-                        int64_t cb, int64_t r0, int64_t r1, int64_t c0, int64_t cend,
-                        bool full_cols) {
+                        int64_t cb, int r0, int r1, int64_t c0, int64_t cend, bool full_cols) {
   constexpr int NW = NT / 32;
-  constexpr int SHIFT = BT & 1;  // (c0 - BT) - even load start
+  constexpr int SHIFT = 0;  // window start is even for every depth (see s2d5_tile)
+  constexpr int EP = EdgeLayout<BT, NT, XS>::kPerPar;
+  const double* eprev = edge + (par ^ 1) * EP;  // written at k-1
+  double* ecur = edge + par * EP;
+  const int tid = threadIdx.x;
+  // XS layout: [level][L=0 / R=1][NT+2], thread t at index t+1
+  auto xs_l = [&](double* base, int L) { return base + (L * 2 + 0) * (NT + 2); };
+  auto xs_r = [&](double* base, int L) { return base + (L * 2 + 1) * (NT + 2); };
   // ---- level 0: input row k
   {
     constexpr int s = smod3(P);
-    const double* src = ring_row + SHIFT + threadIdx.x * C;
+    const double* src = ring_row + SHIFT + tid * C;
     if constexpr (SHIFT == 0 && C % 2 == 0) {
 #pragma unroll
       for (int c = 0; c < C; c += 2) {
@@ -91,24 +107,30 @@ PCOT_DEV void s2d5_iter(Regs<BT, C>& R, const double* __restrict__ ring_row, int
 #pragma unroll
       for (int c = 0; c < C; ++c) R.v[0][s][c] = src[c];
     }
+    if constexpr (XS) {
+      xs_l(ecur, 0)[tid + 1] = R.v[0][s][0];
+      xs_r(ecur, 0)[tid + 1] = R.v[0][s][C - 1];
+    }
   }
-  const double* eprev = edge + (par ^ 1) * (NW * 2 * BT);  // written at k-1
-  double* ecur = edge + par * (NW * 2 * BT);
 #pragma unroll
   for (int L = 0; L < BT; ++L) {
-    constexpr int dummy = 0;
-    (void)dummy;
     const int sm = smod3(P - L - 1);
     const int st = smod3(P - L - 2);
     const int sb = smod3(P - L);
     const double* top = R.v[L][st];
     const double* mid = R.v[L][sm];
     const double* bot = R.v[L][sb];
-    double W = __shfl_up_sync(0xffffffffu, mid[C - 1], 1);
-    double E = __shfl_down_sync(0xffffffffu, mid[0], 1);
-    if (lane == 0 && warp > 0) W = eprev[((warp - 1) * 2 + 1) * BT + L];
-    if (lane == 31 && warp + 1 < NW) E = eprev[((warp + 1) * 2 + 0) * BT + L];
-    const int64_t rho = k - L - 1;
+    double W, E;
+    if constexpr (XS) {
+      W = xs_r(const_cast<double*>(eprev), L)[tid];
+      E = xs_l(const_cast<double*>(eprev), L)[tid + 2];
+    } else {
+      W = __shfl_up_sync(0xffffffffu, mid[C - 1], 1);
+      E = __shfl_down_sync(0xffffffffu, mid[0], 1);
+      if (lane == 0 && warp > 0) W = eprev[((warp - 1) * 2 + 1) * BT + L];
+      if (lane == 31 && warp + 1 < NW) E = eprev[((warp + 1) * 2 + 0) * BT + L];
+    }
+    const int rho = k - L - 1;
     double nv[C];
 #pragma unroll
     for (int c = 0; c < C; ++c) {
@@ -133,8 +155,12 @@ PCOT_DEV void s2d5_iter(Regs<BT, C>& R, const double* __restrict__ ring_row, int
     if (L + 1 < BT) {
 #pragma unroll
       for (int c = 0; c < C; ++c) R.v[L + 1 < BT ? L + 1 : 0][sm][c] = nv[c];
+      if constexpr (XS) {
+        xs_l(ecur, L + 1)[tid + 1] = nv[0];
+        xs_r(ecur, L + 1)[tid + 1] = nv[C - 1];
+      }
     } else if (rho >= r0 && rho < r1) {
-      double* dst = a.out + rho * a.ld_out + cb;
+      double* dst = a.out + int64_t(rho) * a.ld_out + cb;
       if (SHIFT == 0 && C % 2 == 0 && full_cols) {
 #pragma unroll
         for (int c = 0; c < C; c += 2)
@@ -149,29 +175,34 @@ PCOT_DEV void s2d5_iter(Regs<BT, C>& R, const double* __restrict__ ring_row, int
     }
   }
   // ---- publish this iteration's newest row edges of every level (rows k-L)
-  if (lane == 0) {
+  if constexpr (!XS) {
+    if (lane == 0) {
 #pragma unroll
-    for (int L = 0; L < BT; ++L) ecur[(warp * 2 + 0) * BT + L] = R.v[L][smod3(P - L)][0];
-  }
-  if (lane == 31) {
+      for (int L = 0; L < BT; ++L) ecur[(warp * 2 + 0) * BT + L] = R.v[L][smod3(P - L)][0];
+    }
+    if (lane == 31) {
 #pragma unroll
-    for (int L = 0; L < BT; ++L) ecur[(warp * 2 + 1) * BT + L] = R.v[L][smod3(P - L)][C - 1];
+      for (int L = 0; L < BT; ++L) ecur[(warp * 2 + 1) * BT + L] = R.v[L][smod3(P - L)][C - 1];
+    }
   }
 }
 
-template <int BT, int C, int NT, bool MASK, bool HOLD>
+template <int BT, int C, int NT, bool MASK, bool HOLD, bool XS, int kPF>
 PCOT_DEV void s2d5_tile(const S2Args& a, int strip, int chunk, double* ring, uint64_t* bars,
                         double* edge) {
   constexpr int W_LOAD = NT * C + 2;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int64_t c0 = int64_t(strip) * a.w_out;
-  const int64_t cend = c0 + a.w_out < a.cols ? c0 + a.w_out : a.cols;
-  const int64_t r0 = a.row_lo + int64_t(chunk) * a.H;
-  const int64_t r1 = r0 + a.H < a.row_hi ? r0 + a.H : a.row_hi;
-  const int64_t kstart = r0 - BT;
-  const int64_t niter = ((r1 + BT - kstart) + 2) / 3 * 3;
-  const int64_t cfirst = c0 - BT;
-  const int64_t cs = cfirst - (BT & 1);  // even: 16-B aligned bulk copy source
+  // Strips start at s*W_OUT - (BT&1) so the window start (strip - BT) is even
+  // for every depth: 16-B aligned TMA source, vector LDS/STG per thread.
+  const int64_t cstrip = int64_t(strip) * a.w_out - (BT & 1);
+  const int64_t c0 = cstrip < 0 ? 0 : cstrip;
+  const int64_t cend = cstrip + a.w_out < a.cols ? cstrip + a.w_out : a.cols;
+  const int r0 = int(a.row_lo) + chunk * a.H;
+  const int r1 = r0 + a.H < int(a.row_hi) ? r0 + a.H : int(a.row_hi);
+  const int kstart = r0 - BT;
+  const int niter = ((r1 + BT - kstart) + 2) / 3 * 3;
+  const int64_t cfirst = cstrip - BT;
+  const int64_t cs = cfirst;  // even
   const int64_t cb = cfirst + tid * C;
   const bool full_cols = cb >= c0 && cb + C <= cend;
 
@@ -195,17 +226,17 @@ PCOT_DEV void s2d5_tile(const S2Args& a, int strip, int chunk, double* ring, uin
 
   // Every warp waits on the row's mbarrier itself (measured faster than one
   // waiter + the barrier: the try_wait latency then overlaps across warps).
-  for (int64_t it = 0; it < niter; it += 3) {
-#define PCOT_S2_STEP(P)                                                                      \
-  {                                                                                          \
-    const int64_t itp = it + P;                                                              \
-    const int slot = int(itp % kPF);                                                         \
-    mbar_wait(&bars[slot], uint32_t((itp / kPF) & 1));                                       \
-    s2d5_iter<BT, C, NT, MASK, HOLD, P>(R, ring + slot * W_LOAD, kstart + itp, int(itp & 1), \
-                                        edge, warp, lane, a, cb, r0, r1, c0, cend,            \
-                                        full_cols);                                          \
-    __syncthreads();                                                                         \
-    if (tid == 0 && itp + kPF < niter) issue(itp + kPF);                                     \
+  for (int it = 0; it < niter; it += 3) {
+#define PCOT_S2_STEP(P)                                                                    \
+  {                                                                                        \
+    const int itp = it + P;                                                                \
+    const int slot = itp % kPF;                                                            \
+    mbar_wait(&bars[slot], uint32_t((itp / kPF) & 1));                                     \
+    s2d5_iter<BT, C, NT, MASK, HOLD, XS, P>(R, ring + slot * W_LOAD, kstart + itp, itp & 1, \
+                                            edge, warp, lane, a, cb, r0, r1, c0, cend,      \
+                                            full_cols);                                    \
+    __syncthreads();                                                                       \
+    if (tid == 0 && itp + kPF < niter) issue(itp + kPF);                                   \
   }
     PCOT_S2_STEP(0)
     PCOT_S2_STEP(1)
@@ -214,13 +245,19 @@ PCOT_DEV void s2d5_tile(const S2Args& a, int strip, int chunk, double* ring, uin
   }
 }
 
-template <int BT, int C, int NT, int MINB, bool HOLD>
+template <int MINB>
+__host__ __device__ constexpr int ring_depth() {
+  return MINB >= 4 ? 4 : 8;  // rows in flight; 4 CTAs/SM must fit in 228 KB
+}
+
+template <int BT, int C, int NT, int MINB, bool HOLD, bool XS>
 __global__ void __launch_bounds__(NT, MINB) s2d5_kernel(S2Args a) {
   constexpr int W_LOAD = NT * C + 2;
+  constexpr int kPF = ring_depth<MINB>();
   extern __shared__ __align__(128) double smem2[];
   double* ring = smem2;
   double* edge = ring + kPF * W_LOAD;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(edge + 2 * (NT / 32) * 2 * BT);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(edge + EdgeLayout<BT, NT, XS>::kDoubles);
   int strip, chunk;
   if (!tile_coords(blockIdx.x, a.nstrips, a.nchunks, a.order, strip, chunk)) return;
   if (threadIdx.x == 0) {
@@ -228,16 +265,16 @@ __global__ void __launch_bounds__(NT, MINB) s2d5_kernel(S2Args a) {
     fence_mbar_init();
   }
   __syncthreads();
-  const int64_t c0 = int64_t(strip) * a.w_out;
+  const int64_t c0 = int64_t(strip) * a.w_out - (BT & 1);
   const int64_t r0 = a.row_lo + int64_t(chunk) * a.H;
   const int64_t r1 = r0 + a.H < a.row_hi ? r0 + a.H : a.row_hi;
   // Tiles whose dependence cone touches the ring (or the outside) need the masked body.
   const bool edge_tile = (c0 - BT <= 0) || (c0 + a.w_out + BT >= a.cols - 1) ||
                          (a.g0 + r0 - BT <= 0) || (a.g0 + r1 + BT >= a.nrows - 1);
   if (edge_tile)
-    s2d5_tile<BT, C, NT, true, HOLD>(a, strip, chunk, ring, bars, edge);
+    s2d5_tile<BT, C, NT, true, HOLD, XS, kPF>(a, strip, chunk, ring, bars, edge);
   else
-    s2d5_tile<BT, C, NT, false, HOLD>(a, strip, chunk, ring, bars, edge);
+    s2d5_tile<BT, C, NT, false, HOLD, XS, kPF>(a, strip, chunk, ring, bars, edge);
 }
 
 // Pick the chunk height so the grid fills whole waves of resident CTAs:
@@ -258,11 +295,13 @@ void size_grid(S2Args& a, int bt, int rows, int slots) {
   a.H = (rows + best_n - 1) / best_n;
 }
 
-template <int BT, int C, int NT, int MINB>
+template <int BT, int C, int NT, int MINB, bool XS>
 cudaError_t launch_cfg(S2Args a, int ring_hold, int rows, cudaStream_t stream) {
-  auto kern = ring_hold ? s2d5_kernel<BT, C, NT, MINB, true> : s2d5_kernel<BT, C, NT, MINB, false>;
-  constexpr size_t smem = size_t(kPF) * (NT * C + 2) * 8 + size_t(2) * (NT / 32) * 2 * BT * 8 +
-                          size_t(kPF) * 8;
+  auto kern = ring_hold ? s2d5_kernel<BT, C, NT, MINB, true, XS>
+                        : s2d5_kernel<BT, C, NT, MINB, false, XS>;
+  constexpr int kPF = ring_depth<MINB>();
+  constexpr size_t smem = size_t(kPF) * (NT * C + 2) * 8 +
+                          size_t(EdgeLayout<BT, NT, XS>::kDoubles) * 8 + size_t(kPF) * 8;
   static int slots[2] = {0, 0};
   int& sl = slots[ring_hold ? 1 : 0];
   if (sl == 0) {
@@ -275,7 +314,7 @@ cudaError_t launch_cfg(S2Args a, int ring_hold, int rows, cudaStream_t stream) {
     sl = (occ > 0 ? occ : 1) * (sms > 0 ? sms : 148);
   }
   a.w_out = NT * C - 2 * BT;
-  a.nstrips = int((a.cols + a.w_out - 1) / a.w_out);
+  a.nstrips = int((a.cols + (BT & 1) + a.w_out - 1) / a.w_out);
   size_grid(a, BT, rows, sl);
   int grid;
   if (a.order == kOrderMorton) {
@@ -294,13 +333,18 @@ cudaError_t launch_cfg(S2Args a, int ring_hold, int rows, cudaStream_t stream) {
 // selects another for tuning.
 template <int BT>
 cudaError_t launch_bt(const S2Args& a, int ring_hold, int rows, int variant, cudaStream_t s) {
-  if (variant < 0)  // measured best per depth (tools/kbench.py s2d5; profiles/)
-    variant = (BT == 5 || BT == 6) && !ring_hold ? 3 : 0;
+  if (variant < 0)  // measured best per depth (tools/kbench.py s2d5; profiles/kbench_r01.md)
+    variant = BT <= 5 ? 6 : BT == 6 ? 5 : 4;
   switch (variant) {
-    case 1: return launch_cfg<BT, 2, 256, 2>(a, ring_hold, rows, s);
-    case 2: return launch_cfg<BT, 4, 256, 1>(a, ring_hold, rows, s);
-    case 3: return launch_cfg<BT, 4, 128, 3>(a, ring_hold, rows, s);
-    default: return launch_cfg<BT, 4, 128, 2>(a, ring_hold, rows, s);
+    case 1: return launch_cfg<BT, 2, 256, 2, false>(a, ring_hold, rows, s);
+    case 2: return launch_cfg<BT, 4, 256, 1, false>(a, ring_hold, rows, s);
+    case 3: return launch_cfg<BT, 4, 128, 3, false>(a, ring_hold, rows, s);
+    case 4: return launch_cfg<BT, 4, 128, 2, true>(a, ring_hold, rows, s);
+    case 5: return launch_cfg<BT, 4, 128, 3, true>(a, ring_hold, rows, s);
+    case 6: return launch_cfg<BT, 4, 128, 4, true>(a, ring_hold, rows, s);
+    case 7: return launch_cfg<BT, 2, 256, 2, true>(a, ring_hold, rows, s);
+    case 8: return launch_cfg<BT, 2, 128, 4, true>(a, ring_hold, rows, s);
+    default: return launch_cfg<BT, 4, 128, 2, false>(a, ring_hold, rows, s);
   }
 }
 

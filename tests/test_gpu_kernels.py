@@ -68,7 +68,7 @@ def test_sharded_slabs_equal_single_grid_on_one_gpu():
     assert np.array_equal(split.view(np.uint64), want.view(np.uint64))
 
 
-@pytest.mark.parametrize("variant", [0, 1, 2, 3])
+@pytest.mark.parametrize("variant", [0, 1, 2, 3, 4, 5])
 def test_s2d5_variants_bit_exact(variant, monkeypatch):
     """Every compiled (C, NT, MINB) variant of the 2-D kernel, all depths."""
     import subprocess

@@ -1,4 +1,4 @@
 cd $GRAFT_REPO_ROOT
-PCOTGPU_S2D5_VARIANT=0 timeout 300 python tools/kbench.py s2d5 --rows 8192 --bts 7 --orders slt > gpurun_out/kb_plain.log 2>&1 && \
-PCOTGPU_S2D5_VARIANT=0 timeout 900 ncu --set full --import-source on --clock-control none -k regex:s2d5 -s 1 -c 1 -o gpurun_out/prof_s2d5_v0_bt7 python tools/kbench.py s2d5 --rows 8192 --bts 7 --orders slt > gpurun_out/ncu_s2d5.log 2>&1
-echo "ncu rc=$?"; cat gpurun_out/kb_plain.log
+timeout 900 python -m pytest tests/test_gpu_kernels.py tests/test_gpu_parity.py -q -m gpu -x -k "variants or jacobi or heat2d or sharded or storage or host" > gpurun_out/pytest_v.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_v.log
+for v in 5 6 8; do echo "variant $v"; PCOTGPU_S2D5_VARIANT=$v timeout 300 python tools/kbench.py s2d5 --bts 3,4,5,6,7 --orders slt 2>&1 | grep -v Warn; done > gpurun_out/kb_variants5.log 2>&1
+tail -3 gpurun_out/pytest_v.log; cat gpurun_out/kb_variants5.log
