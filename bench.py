@@ -51,15 +51,24 @@ def peak_hbm():
         return 6650.0, "fallback (B200_PROFILING.md)"
 
 
-def ncu_traffic():
-    """dram bytes per s2d5 launch from the committed ncu --set full summary."""
-    p = os.path.join(REPO, "profiles", "ncu_s2d5_summary.json")
-    try:
-        with open(p) as f:
-            d = json.load(f)
-        return d.get("dram_bytes_per_launch_scaled_to_bench")
-    except Exception:
-        return None
+def ncu_traffic(bt, cells):
+    """dram__bytes_read.sum + dram__bytes_write.sum per s2d5 launch, from the
+    committed `ncu --set full` capture of this bench command at this depth
+    (profiles/ncu_bench_s2d5_bt<bt>_r*.json; tools/ncu_summary.py)."""
+    import glob
+
+    for p in sorted(glob.glob(os.path.join(REPO, "profiles", "ncu_bench_s2d5_bt%d_r*.json" % bt)),
+                    reverse=True):
+        try:
+            with open(p) as f:
+                d = json.load(f)
+            if abs(d.get("algorithmic_bytes", 0) - 16.0 * cells) < 1:
+                return {"bytes_per_launch": d["dram_bytes"],
+                        "over_algorithmic": d.get("traffic_over_algorithmic"),
+                        "source": os.path.relpath(p, REPO)}
+        except Exception:
+            continue
+    return None
 
 
 class ClockSampler:
@@ -267,9 +276,12 @@ def main():
     kernel_ms = sum(kms) / args.steps  # summed launch time per step
     peak, peak_src = peak_hbm()
     achieved = bytes_per_run / (kernel_ms / 1e3) / 1e9 if kernel_ms > 0 else None
-    traffic = ncu_traffic()
+    traffic = ncu_traffic(args.bt, cells) if world == 1 else None
     roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-            "frac": (achieved / peak) if achieved else None, "traffic": traffic,
+            "frac": (achieved / peak) if achieved else None,
+            "traffic": traffic["bytes_per_launch"] if traffic else None,
+            "traffic_source": traffic,
+            "algorithmic_bytes_per_launch": 16.0 * cells,
             "kernel": "s2d5_kernel<bt=%d>" % args.bt, "peak_source": peak_src,
             "avg_launch_ms": (sum(kms) / len(kms)) if kms else None,
             "launches_per_step": len(kms) // max(1, args.steps),
