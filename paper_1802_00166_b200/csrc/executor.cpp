@@ -231,8 +231,9 @@ struct GpuExecutor::Impl {
   }
 
   int run_gs(const TileOrder& o) {
-    int bt = env_int("PCOTGPU_GS_BT", 4), bx = env_int("PCOTGPU_GS_BX", 32),
-        by = env_int("PCOTGPU_GS_BY", 256);
+    // default tile = best measured (profiles/kbench_r01.md)
+    int bt = env_int("PCOTGPU_GS_BT", 2), bx = env_int("PCOTGPU_GS_BX", 64),
+        by = env_int("PCOTGPU_GS_BY", 64);
     if (o.scheme != Scheme::Untiled && o.tile.leaf.size() >= 3) {
       bt = int(o.tile.leaf[0]);
       bx = int(o.tile.leaf[1]);

@@ -142,6 +142,95 @@ __global__ void gs2d_kernel(GsArgs g) {
   }
 }
 
+// One warp per tile (bt * bx == 32): the per-clock ordering is a __syncwarp
+// instead of a CTA barrier, the line's own previous value stays in a
+// register (off the shared-memory round trip), and only the final version of
+// every cell the tile wrote goes back to global memory (a byte mask marks
+// written cells).  Intermediate versions are consumed inside the tile only:
+// by the universal occupancy vector, any version read outside the tile that
+// produced it is that tile's last version of the cell.
+__global__ void __launch_bounds__(32) gs2d_warp_kernel(GsArgs g) {
+  extern __shared__ __align__(16) double reg[];
+  const int cells = g.ni * g.ns;
+  unsigned char* wr = reinterpret_cast<unsigned char*>(reg + cells);
+  const int lane = threadIdx.x;
+  const int tt = lane / g.bx, xx = lane - (lane / g.bx) * g.bx;
+  const int nclk = g.bt + g.bx + g.by - 2;
+  for (;;) {
+    int tile = 0;
+    if (lane == 0) tile = atomicAdd(g.counter, 1);
+    tile = __shfl_sync(0xffffffffu, tile, 0);
+    if (tile >= g.ntiles) return;
+    const int tb = g.tiles[tile * 3 + 0], xb = g.tiles[tile * 3 + 1], yb = g.tiles[tile * 3 + 2];
+    if (lane < 8) {
+      const int p = g.preds[tile * 8 + lane];
+      if (p >= 0)
+        while (ld_acquire(g.flags + p) == 0) __nanosleep(32);
+    }
+    __syncwarp();
+    const int t0 = 1 + tb * g.bt;
+    const int x0 = 2 + xb * g.bx;
+    const int y0 = 4 + yb * g.by;
+    const int I0 = x0 - t0 - g.bt;
+    const int S0 = y0 - 2 * t0 - 2 * g.bt;
+    for (int e = lane; e < cells; e += 32) {
+      const int r = e / g.ns, c = e - r * g.ns;
+      const int i = I0 + r, j = S0 + c - i;
+      double v = 0.0;
+      if (i >= 0 && i < g.n && j >= 0 && j < g.n) v = ld_cg(g.a + int64_t(i) * g.ld + j);
+      reg[e] = v;
+      wr[e] = 0;
+    }
+    __syncwarp();
+    const int t = t0 + tt, i = x0 + xx - t;
+    const bool line_ok = t <= g.T && i >= 1 && i <= g.n - 2;
+    const int ri = i - I0;
+    // s = y - 2t = y0 + clk - tt - xx - 2t ; column in the region = s - S0
+    const int cs0 = y0 - tt - xx - 2 * t - S0;  // region column at clk = 0
+    const int j0 = y0 - tt - xx - 2 * t - i;     // j at clk = 0
+    double* row = reg + ri * g.ns;
+    double prev = 0.0;
+    bool have_prev = false;
+    for (int clk = 0; clk < nclk; ++clk) {
+      const int yy = clk - tt - xx;
+      const int j = j0 + clk;
+      if (line_ok && yy >= 0 && yy < g.by && j >= 1 && j <= g.n - 2) {
+        const int cs = cs0 + clk;
+        const double* up = row - g.ns + cs;
+        double* me = row + cs;
+        const double* dn = row + g.ns + cs;
+        const double b = have_prev ? prev : me[-1];
+        double acc = add(up[-2], up[-1]);
+        acc = add(acc, up[0]);
+        acc = add(acc, b);
+        acc = add(acc, me[0]);
+        acc = add(acc, me[1]);
+        acc = add(acc, dn[0]);
+        acc = add(acc, dn[1]);
+        acc = add(acc, dn[2]);
+        const double v = div9(acc);
+        me[0] = v;
+        wr[ri * g.ns + cs] = 1;
+        prev = v;
+        have_prev = true;
+      } else {
+        have_prev = false;
+      }
+      __syncwarp();
+    }
+    for (int e = lane; e < cells; e += 32) {
+      if (wr[e]) {
+        const int r = e / g.ns, c = e - r * g.ns;
+        const int ii = I0 + r, jj = S0 + c - ii;
+        g.a[int64_t(ii) * g.ld + jj] = reg[e];
+      }
+    }
+    __threadfence();
+    __syncwarp();
+    if (lane == 0) st_release(g.flags + tile, 1);
+  }
+}
+
 }  // namespace
 
 GsPlan* gs2d_plan_create(int64_t n, int64_t T, int bt, int bx, int by, int device) {
@@ -197,10 +286,12 @@ GsPlan* gs2d_plan_create(int64_t n, int64_t T, int bt, int bx, int by, int devic
   cudaMemcpy(p->d_tiles, tiles.data(), tiles.size() * sizeof(int), cudaMemcpyHostToDevice);
   cudaMemcpy(p->d_preds, preds.data(), preds.size() * sizeof(int), cudaMemcpyHostToDevice);
   const int ni = bx + bt + 1, ns = by + 2 * bt + 2;
-  const size_t smem = size_t(ni) * ns * 8;
-  cudaFuncSetAttribute(gs2d_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  const bool warp = bt * bx == 32;
+  const size_t smem = size_t(ni) * ns * (warp ? 9 : 8) + 16;
+  auto kern = warp ? gs2d_warp_kernel : gs2d_kernel;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
   int occ = 0, sms = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, gs2d_kernel, bt * bx, smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, bt * bx, smem);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
   p->grid = int(std::max<int64_t>(1, std::min<int64_t>(p->ntiles, int64_t(occ) * sms)));
   return p;
@@ -242,8 +333,12 @@ cudaError_t gs2d_run(GsPlan* p, double* a, int64_t ld, cudaStream_t stream) {
   g.preds = p->d_preds;
   g.flags = p->d_state;
   g.counter = p->d_state + p->ntiles;
-  const size_t smem = size_t(g.ni) * g.ns * 8;
-  gs2d_kernel<<<p->grid, p->bt * p->bx, smem, stream>>>(g);
+  const bool warp = p->bt * p->bx == 32;
+  const size_t smem = size_t(g.ni) * g.ns * (warp ? 9 : 8) + 16;
+  if (warp)
+    gs2d_warp_kernel<<<p->grid, 32, smem, stream>>>(g);
+  else
+    gs2d_kernel<<<p->grid, p->bt * p->bx, smem, stream>>>(g);
   count_launch();
   return cudaGetLastError();
 }

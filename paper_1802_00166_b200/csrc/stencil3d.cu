@@ -4,16 +4,22 @@
 // 347-428; kernels/heat3d.kernel:34 and this repo's kernels/heat3d_b.kernel).
 //
 // Tile = a (j,k) plane window of KW x JW input cells streamed along i:
-//   * lane -> C consecutive k columns, warp -> RJ consecutive j rows;
+//   * lane -> C consecutive k columns, warp -> RJ consecutive j rows; a warp
+//     spans the whole window width, so k-neighbours come by warp shuffle with
+//     no cross-warp traffic (lanes 0/31 read the shrinking halo);
 //   * input planes arrive through a PF-deep shared-memory ring (one TMA bulk
 //     copy per j row, issued by warp 0, mbarrier complete_tx);
 //   * level L keeps planes rho-1, rho, rho+1 (slot = plane mod 3) in
-//     registers; k-neighbours come by warp shuffle, j-neighbours inside the
-//     thread or, at warp edges, through a double-buffered shared-memory row
-//     exchange (one __syncthreads per input plane).
+//     registers; j-neighbours inside the thread or, at warp edges, through a
+//     double-buffered shared-memory row exchange (one __syncthreads per plane).
 // The (j,k) window shrinks by one cell per level: output KW-2BT x JW-2BT.
+// Ring handling: tiles whose window stays inside the interior in (j,k) run
+// the unmasked body; planes at i = 0 / N-1 (or outside) are handled by a
+// warp-uniform branch; only (j,k)-edge tiles pay per-element selects.
 // Per-point order = the kernel body's parse tree (neighbours (i-1),(i+1),
 // (j-1),(j+1),(k-1),(k+1)); explicit _rn intrinsics, no FMA.
+#include <cstdlib>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -21,29 +27,31 @@ namespace pcotgpu {
 
 namespace {
 
-constexpr int kC3 = 2;               // k columns per thread
-constexpr int kRJ = 4;               // j rows per thread
-constexpr int kNW3 = 8;              // warps per CTA
-constexpr int kNT3 = kNW3 * 32;
-constexpr int kKW = 32 * kC3;        // 64 input k columns
-constexpr int kJW = kNW3 * kRJ;      // 32 input j rows
-constexpr int kKL = kKW + 2;         // loaded row length (alignment slack)
-constexpr int kPF3 = 4;              // planes in flight
+template <int C_, int RJ_, int NW_, int MINB_, int PF_>
+struct Geo {
+  static constexpr int C = C_, RJ = RJ_, NW = NW_, MINB = MINB_, PF = PF_;
+  static constexpr int NT = NW * 32;
+  static constexpr int KW = 32 * C;   // input k columns
+  static constexpr int JW = NW * RJ;  // input j rows
+  static constexpr int KL = KW + 2;   // loaded row length (alignment slack)
+};
 
 struct S3Args {
   const double* in;
   double* out;
-  int64_t n;
+  int n;
   int64_t pj_in, pi_in, pj_out, pi_out;
-  int64_t halo;
+  int halo;
   int kout, jout;
   int nk, nj, nchunks, H;
   int order;
 };
 
-template <int BT>
+__host__ __device__ constexpr int m3(int v) { return ((v % 3) + 3) % 3; }
+
+template <int BT, class G>
 struct Regs3 {
-  double v[BT][3][kRJ][kC3];
+  double v[BT][3][G::RJ][G::C];
 };
 
 template <int RULE>
@@ -68,159 +76,164 @@ PCOT_DEV double update7(double c, double im, double ip, double jm, double jp, do
   }
 }
 
-template <int BT, int RULE, bool MASK, bool HOLD, int P>
-PCOT_DEV void s3_iter(Regs3<BT>& R, const double* __restrict__ plane, int shift, int64_t k,
-                      int par, double* __restrict__ edge, int warp, int lane, const S3Args& a,
-                      int64_t jb, int64_t kb, int64_t i0, int64_t i1, int64_t j0, int64_t jend,
-                      int64_t k0, int64_t kend) {
-  // edge layout: [par][warp][top/bottom][L][lane][C]
-  constexpr int EW = 2 * BT * 32 * kC3;  // doubles per warp
+// edge layout per parity: [warp][top=0/bottom=1][L][lane][C]
+template <int BT, class G>
+struct Edge3 {
+  static constexpr int EW = 2 * BT * 32 * G::C;  // doubles per warp
+  static constexpr int kPerPar = G::NW * EW;
+};
+
+template <int BT, int RULE, bool MASKJK, bool HOLD, class G, int P>
+PCOT_DEV void s3_iter(Regs3<BT, G>& R, const double* __restrict__ plane, int shift, int k, int par,
+                      double* __restrict__ edge, int warp, int lane, const S3Args& a, int jb,
+                      int kb, unsigned jkmask, int i0, int i1, int j0, int jend, int k0, int kend) {
+  constexpr int C = G::C, RJ = G::RJ, NW = G::NW;
+  constexpr int EW = Edge3<BT, G>::EW;
   {
-    constexpr int s = P % 3;
+    constexpr int s = m3(P);
 #pragma unroll
-    for (int r = 0; r < kRJ; ++r)
+    for (int r = 0; r < RJ; ++r)
 #pragma unroll
-      for (int c = 0; c < kC3; ++c)
-        R.v[0][s][r][c] = plane[(warp * kRJ + r) * kKL + shift + lane * kC3 + c];
+      for (int c = 0; c < C; ++c)
+        R.v[0][s][r][c] = plane[(warp * RJ + r) * G::KL + shift + lane * C + c];
   }
-  const double* eprev = edge + (par ^ 1) * (kNW3 * EW);
+  const double* eprev = edge + (par ^ 1) * Edge3<BT, G>::kPerPar;
 #pragma unroll
   for (int L = 0; L < BT; ++L) {
-    const int rel = P - L - 1;
-    const int sm = ((rel % 3) + 3) % 3;
-    const int st = (((rel - 1) % 3) + 3) % 3;
-    const int sb = (((rel + 1) % 3) + 3) % 3;
-    const int64_t rho = k - L - 1;
-    // j-neighbours beyond this warp's rows
-    double up[kC3], dn[kC3];
+    const int sm = m3(P - L - 1), st = m3(P - L - 2), sb = m3(P - L);
+    const int rho = k - L - 1;
+    double up[C], dn[C];
 #pragma unroll
-    for (int c = 0; c < kC3; ++c) {
-      up[c] = R.v[L][sm][0][c];
-      dn[c] = R.v[L][sm][kRJ - 1][c];
+    for (int c = 0; c < C; ++c) {
+      up[c] = warp > 0 ? eprev[(warp - 1) * EW + ((1 * BT + L) * 32 + lane) * C + c]
+                       : R.v[L][sm][0][c];
+      dn[c] = warp + 1 < NW ? eprev[(warp + 1) * EW + ((0 * BT + L) * 32 + lane) * C + c]
+                            : R.v[L][sm][RJ - 1][c];
     }
-    if (warp > 0) {
+    double nv[RJ][C];
 #pragma unroll
-      for (int c = 0; c < kC3; ++c)
-        up[c] = eprev[(warp - 1) * EW + ((1 * BT + L) * 32 + lane) * kC3 + c];
-    }
-    if (warp + 1 < kNW3) {
-#pragma unroll
-      for (int c = 0; c < kC3; ++c)
-        dn[c] = eprev[(warp + 1) * EW + ((0 * BT + L) * 32 + lane) * kC3 + c];
-    }
-    double nv[kRJ][kC3];
-#pragma unroll
-    for (int r = 0; r < kRJ; ++r) {
+    for (int r = 0; r < RJ; ++r) {
       const double* mid = R.v[L][sm][r];
-      double W = __shfl_up_sync(0xffffffffu, mid[kC3 - 1], 1);
-      double E = __shfl_down_sync(0xffffffffu, mid[0], 1);
+      const double W = __shfl_up_sync(0xffffffffu, mid[C - 1], 1);
+      const double E = __shfl_down_sync(0xffffffffu, mid[0], 1);
 #pragma unroll
-      for (int c = 0; c < kC3; ++c) {
+      for (int c = 0; c < C; ++c) {
         const double jm = r > 0 ? R.v[L][sm][r > 0 ? r - 1 : 0][c] : up[c];
-        const double jp = r < kRJ - 1 ? R.v[L][sm][r < kRJ - 1 ? r + 1 : 0][c] : dn[c];
+        const double jp = r < RJ - 1 ? R.v[L][sm][r < RJ - 1 ? r + 1 : 0][c] : dn[c];
         const double km = c > 0 ? mid[c > 0 ? c - 1 : 0] : W;
-        const double kp = c < kC3 - 1 ? mid[c < kC3 - 1 ? c + 1 : 0] : E;
+        const double kp = c < C - 1 ? mid[c < C - 1 ? c + 1 : 0] : E;
         nv[r][c] = update7<RULE>(mid[c], R.v[L][st][r][c], R.v[L][sb][r][c], jm, jp, km, kp);
       }
     }
-    if (MASK) {
-      const bool iin = rho >= 1 && rho <= a.n - 2;
+    if (MASKJK) {
 #pragma unroll
-      for (int r = 0; r < kRJ; ++r) {
-        const int64_t j = jb + r;
-        const bool jin = iin && j >= 1 && j <= a.n - 2;
+      for (int r = 0; r < RJ; ++r)
 #pragma unroll
-        for (int c = 0; c < kC3; ++c) {
-          const int64_t kk = kb + c;
-          if (!(jin && kk >= 1 && kk <= a.n - 2)) nv[r][c] = HOLD ? R.v[L][sm][r][c] : 0.0;
-        }
-      }
+        for (int c = 0; c < C; ++c)
+          if (!((jkmask >> (r * C + c)) & 1u)) nv[r][c] = HOLD ? R.v[L][sm][r][c] : 0.0;
+    }
+    if (rho < 1 || rho > a.n - 2) {  // ring / outside plane: warp-uniform
+#pragma unroll
+      for (int r = 0; r < RJ; ++r)
+#pragma unroll
+        for (int c = 0; c < C; ++c) nv[r][c] = HOLD ? R.v[L][sm][r][c] : 0.0;
     }
     if (L + 1 < BT) {
 #pragma unroll
-      for (int r = 0; r < kRJ; ++r)
+      for (int r = 0; r < RJ; ++r)
 #pragma unroll
-        for (int c = 0; c < kC3; ++c) R.v[L + 1 < BT ? L + 1 : 0][sm][r][c] = nv[r][c];
+        for (int c = 0; c < C; ++c) R.v[L + 1 < BT ? L + 1 : 0][sm][r][c] = nv[r][c];
     } else if (rho >= i0 && rho < i1) {
 #pragma unroll
-      for (int r = 0; r < kRJ; ++r) {
-        const int64_t j = jb + r;
+      for (int r = 0; r < RJ; ++r) {
+        const int j = jb + r;
         if (j < j0 || j >= jend) continue;
-        double* dst = a.out + rho * a.pi_out + j * a.pj_out;
+        double* dst = a.out + int64_t(rho) * a.pi_out + int64_t(j) * a.pj_out;
 #pragma unroll
-        for (int c = 0; c < kC3; ++c) {
-          const int64_t kk = kb + c;
+        for (int c = 0; c < C; ++c) {
+          const int kk = kb + c;
           if (kk >= k0 && kk < kend) __stcs(dst + kk, nv[r][c]);
         }
       }
     }
   }
   // publish top/bottom rows of the newest plane (k-L) of every level
-  double* ecur = edge + par * (kNW3 * EW);
+  double* ecur = edge + par * Edge3<BT, G>::kPerPar;
 #pragma unroll
   for (int L = 0; L < BT; ++L) {
-    const int s = (((P - L) % 3) + 3) % 3;
+    const int s = m3(P - L);
 #pragma unroll
-    for (int c = 0; c < kC3; ++c) {
-      ecur[warp * EW + ((0 * BT + L) * 32 + lane) * kC3 + c] = R.v[L][s][0][c];
-      ecur[warp * EW + ((1 * BT + L) * 32 + lane) * kC3 + c] = R.v[L][s][kRJ - 1][c];
+    for (int c = 0; c < C; ++c) {
+      ecur[warp * EW + ((0 * BT + L) * 32 + lane) * C + c] = R.v[L][s][0][c];
+      ecur[warp * EW + ((1 * BT + L) * 32 + lane) * C + c] = R.v[L][s][RJ - 1][c];
     }
   }
 }
 
-template <int BT, int RULE, bool MASK, bool HOLD>
+template <int BT, int RULE, bool MASKJK, bool HOLD, class G>
 PCOT_DEV void s3_tile(const S3Args& a, int tk, int tj, int chunk, double* ring, uint64_t* bars,
                       double* edge) {
+  constexpr int C = G::C, RJ = G::RJ, JW = G::JW, KL = G::KL, PF = G::PF;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int64_t k0 = int64_t(tk) * a.kout, j0 = int64_t(tj) * a.jout;
-  const int64_t kend = k0 + a.kout < a.n ? k0 + a.kout : a.n;
-  const int64_t jend = j0 + a.jout < a.n ? j0 + a.jout : a.n;
-  const int64_t i0 = int64_t(chunk) * a.H;
-  const int64_t i1 = i0 + a.H < a.n ? i0 + a.H : a.n;
-  const int64_t kstart = i0 - BT;
-  const int64_t niter = ((i1 + BT - kstart) + 2) / 3 * 3;
-  const int64_t kfirst = k0 - BT, jfirst = j0 - BT;
-  const int64_t cs = kfirst >= 0 ? (kfirst & ~int64_t(1)) : -((-kfirst + 1) & ~int64_t(1));
-  const int shift = int(kfirst - cs);
-  const int64_t kb = kfirst + lane * kC3;
-  const int64_t jb = jfirst + warp * kRJ;
-  const int64_t lo = -a.halo, hi = a.n + a.halo - 1;
+  const int k0 = tk * a.kout, j0 = tj * a.jout;
+  const int kend = k0 + a.kout < a.n ? k0 + a.kout : a.n;
+  const int jend = j0 + a.jout < a.n ? j0 + a.jout : a.n;
+  const int i0 = chunk * a.H;
+  const int i1 = i0 + a.H < a.n ? i0 + a.H : a.n;
+  const int kstart = i0 - BT;
+  const int niter = ((i1 + BT - kstart) + 2) / 3 * 3;
+  const int kfirst = k0 - BT, jfirst = j0 - BT;
+  const int cs = kfirst >= 0 ? (kfirst & ~1) : -((-kfirst + 1) & ~1);
+  const int shift = kfirst - cs;
+  const int kb = kfirst + lane * C;
+  const int jb = jfirst + warp * RJ;
+  const int lo = -a.halo, hi = a.n + a.halo - 1;
+  unsigned jkmask = 0;  // interior (j,k) cells of this thread's patch
+#pragma unroll
+  for (int r = 0; r < RJ; ++r)
+#pragma unroll
+    for (int c = 0; c < C; ++c) {
+      const int j = jb + r, kk = kb + c;
+      if (j >= 1 && j <= a.n - 2 && kk >= 1 && kk <= a.n - 2) jkmask |= 1u << (r * C + c);
+    }
 
-  auto issue = [&](int64_t it) {  // warp 0, all lanes
-    int64_t pl = kstart + it;
+  auto issue = [&](int it) {  // warp 0, all lanes
+    int pl = kstart + it;
     pl = pl < lo ? lo : (pl > hi ? hi : pl);
-    const int slot = int(it % kPF3);
-    if (lane == 0) mbar_arrive_expect_tx(&bars[slot], kJW * kKL * 8);
+    const int slot = it % PF;
+    if (lane == 0) mbar_arrive_expect_tx(&bars[slot], JW * KL * 8);
     __syncwarp();
-    int64_t jr = jfirst + lane;
-    jr = jr < lo ? lo : (jr > hi ? hi : jr);
-    bulk_g2s(ring + (slot * kJW + lane) * kKL, a.in + pl * a.pi_in + jr * a.pj_in + cs, kKL * 8,
-             &bars[slot]);
+    for (int row = lane; row < JW; row += 32) {
+      int jr = jfirst + row;
+      jr = jr < lo ? lo : (jr > hi ? hi : jr);
+      bulk_g2s(ring + (slot * JW + row) * KL,
+               a.in + int64_t(pl) * a.pi_in + int64_t(jr) * a.pj_in + cs, KL * 8, &bars[slot]);
+    }
   };
   if (warp == 0) {
-    for (int it = 0; it < kPF3 && it < niter; ++it) issue(it);
+    for (int it = 0; it < PF && it < niter; ++it) issue(it);
   }
-  Regs3<BT> R;
+  Regs3<BT, G> R;
 #pragma unroll
   for (int L = 0; L < BT; ++L)
 #pragma unroll
     for (int s = 0; s < 3; ++s)
 #pragma unroll
-      for (int r = 0; r < kRJ; ++r)
+      for (int r = 0; r < RJ; ++r)
 #pragma unroll
-        for (int c = 0; c < kC3; ++c) R.v[L][s][r][c] = 0.0;
+        for (int c = 0; c < C; ++c) R.v[L][s][r][c] = 0.0;
 
-  for (int64_t it = 0; it < niter; it += 3) {
-#define PCOT_S3_STEP(P)                                                                        \
-  {                                                                                            \
-    const int64_t itp = it + P;                                                                \
-    const int slot = int(itp % kPF3);                                                          \
-    mbar_wait(&bars[slot], uint32_t((itp / kPF3) & 1));                                        \
-    s3_iter<BT, RULE, MASK, HOLD, P>(R, ring + slot * kJW * kKL, shift, kstart + itp,          \
-                                     int(itp & 1), edge, warp, lane, a, jb, kb, i0, i1, j0,    \
-                                     jend, k0, kend);                                          \
-    __syncthreads();                                                                           \
-    if (warp == 0 && itp + kPF3 < niter) issue(itp + kPF3);                                    \
+  for (int it = 0; it < niter; it += 3) {
+#define PCOT_S3_STEP(P)                                                                     \
+  {                                                                                         \
+    const int itp = it + P;                                                                 \
+    const int slot = itp % PF;                                                              \
+    mbar_wait(&bars[slot], uint32_t((itp / PF) & 1));                                       \
+    s3_iter<BT, RULE, MASKJK, HOLD, G, P>(R, ring + slot * JW * KL, shift, kstart + itp,     \
+                                          itp & 1, edge, warp, lane, a, jb, kb, jkmask, i0,  \
+                                          i1, j0, jend, k0, kend);                           \
+    __syncthreads();                                                                        \
+    if (warp == 0 && itp + PF < niter) issue(itp + PF);                                     \
   }
     PCOT_S3_STEP(0)
     PCOT_S3_STEP(1)
@@ -229,12 +242,12 @@ PCOT_DEV void s3_tile(const S3Args& a, int tk, int tj, int chunk, double* ring, 
   }
 }
 
-template <int BT, int RULE, bool HOLD>
-__global__ void __launch_bounds__(kNT3, 1) s3d7_kernel(S3Args a) {
+template <int BT, int RULE, bool HOLD, class G>
+__global__ void __launch_bounds__(G::NT, G::MINB) s3d7_kernel(S3Args a) {
   extern __shared__ __align__(128) double smem3[];
   double* ring = smem3;
-  double* edge = ring + kPF3 * kJW * kKL;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(edge + 2 * kNW3 * 2 * BT * 32 * kC3);
+  double* edge = ring + G::PF * G::JW * G::KL;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(edge + 2 * Edge3<BT, G>::kPerPar);
   const int ntile = a.nk * a.nj;
   int tile = blockIdx.x % ntile, chunk = blockIdx.x / ntile;
   int tk, tj;
@@ -255,29 +268,50 @@ __global__ void __launch_bounds__(kNT3, 1) s3d7_kernel(S3Args a) {
     if (tk >= a.nk || tj >= a.nj) return;
   }
   if (threadIdx.x == 0) {
-    for (int i = 0; i < kPF3; ++i) mbar_init(&bars[i], 1);
+    for (int i = 0; i < G::PF; ++i) mbar_init(&bars[i], 1);
     fence_mbar_init();
   }
   __syncthreads();
-  const int64_t k0 = int64_t(tk) * a.kout, j0 = int64_t(tj) * a.jout;
-  const int64_t i0 = int64_t(chunk) * a.H;
-  const int64_t i1 = i0 + a.H < a.n ? i0 + a.H : a.n;
-  const bool edge_tile = (k0 - BT <= 0) || (k0 + a.kout + BT >= a.n - 1) || (j0 - BT <= 0) ||
-                         (j0 + a.jout + BT >= a.n - 1) || (i0 - BT <= 0) ||
-                         (i1 + BT >= a.n - 1);
-  if (edge_tile)
-    s3_tile<BT, RULE, true, HOLD>(a, tk, tj, chunk, ring, bars, edge);
+  const int k0 = tk * a.kout, j0 = tj * a.jout;
+  const bool edge_jk = (k0 - BT <= 0) || (k0 + a.kout + BT >= a.n - 1) || (j0 - BT <= 0) ||
+                       (j0 + a.jout + BT >= a.n - 1);
+  if (edge_jk)
+    s3_tile<BT, RULE, true, HOLD, G>(a, tk, tj, chunk, ring, bars, edge);
   else
-    s3_tile<BT, RULE, false, HOLD>(a, tk, tj, chunk, ring, bars, edge);
+    s3_tile<BT, RULE, false, HOLD, G>(a, tk, tj, chunk, ring, bars, edge);
 }
 
-template <int BT, int RULE, bool HOLD>
-cudaError_t launch3(const S3Args& a, cudaStream_t stream) {
-  const size_t smem = size_t(kPF3) * kJW * kKL * 8 + size_t(2) * kNW3 * 2 * BT * 32 * kC3 * 8 +
-                      kPF3 * 8;
-  auto fn = s3d7_kernel<BT, RULE, HOLD>;
-  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-  if (e != cudaSuccess) return e;
+template <int BT, int RULE, bool HOLD, class G>
+cudaError_t launch3(S3Args a, cudaStream_t stream) {
+  constexpr size_t smem = size_t(G::PF) * G::JW * G::KL * 8 +
+                          size_t(2) * Edge3<BT, G>::kPerPar * 8 + G::PF * 8;
+  auto fn = s3d7_kernel<BT, RULE, HOLD, G>;
+  static int slots = 0;
+  if (slots == 0) {
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    if (e != cudaSuccess) return e;
+    int occ = 0, sms = 0, dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, G::NT, smem);
+    slots = (occ > 0 ? occ : 1) * (sms > 0 ? sms : 148);
+  }
+  a.kout = G::KW - 2 * BT;
+  a.jout = G::JW - 2 * BT;
+  a.nk = (a.n + a.kout - 1) / a.kout;
+  a.nj = (a.n + a.jout - 1) / a.jout;
+  // chunk height: whole waves of resident CTAs, minimise waves * (H + 2*BT + 2)
+  const int64_t tiles = int64_t(a.nk) * a.nj;
+  int best = 1;
+  double bestc = 1e300;
+  for (int nc = 1; nc <= (a.n / (4 * BT) > 1 ? a.n / (4 * BT) : 1); ++nc) {
+    const int H = (a.n + nc - 1) / nc;
+    const int64_t waves = (tiles * nc + slots - 1) / slots;
+    const double cost = double(waves) * (H + 2 * BT + 2);
+    if (cost < bestc * 0.999) bestc = cost, best = nc;
+  }
+  a.nchunks = best;
+  a.H = (a.n + best - 1) / best;
   int grid;
   if (a.order == kOrderLex) {
     grid = a.nk * a.nj * a.nchunks;
@@ -286,16 +320,29 @@ cudaError_t launch3(const S3Args& a, cudaStream_t stream) {
     while (side < a.nk || side < a.nj) side <<= 1;
     grid = side * side * a.nchunks;
   }
-  fn<<<grid, kNT3, smem, stream>>>(a);
+  fn<<<grid, G::NT, smem, stream>>>(a);
   count_launch();
   return cudaGetLastError();
 }
 
+template <int BT, class G>
+cudaError_t launch3_rule(const S3Args& a, int rule, int hold, cudaStream_t s) {
+  if (rule == 0) return hold ? launch3<BT, 0, true, G>(a, s) : launch3<BT, 0, false, G>(a, s);
+  return hold ? launch3<BT, 1, true, G>(a, s) : launch3<BT, 1, false, G>(a, s);
+}
+
+// Variant table (C, RJ, NW, MINB, PF); PCOTGPU_S3D7_VARIANT selects one.
 template <int BT>
-cudaError_t launch3_bt(const S3Args& a, int rule, int hold, cudaStream_t s) {
-  if (rule == 0)
-    return hold ? launch3<BT, 0, true>(a, s) : launch3<BT, 0, false>(a, s);
-  return hold ? launch3<BT, 1, true>(a, s) : launch3<BT, 1, false>(a, s);
+cudaError_t launch3_bt(const S3Args& a, int rule, int hold, int variant, cudaStream_t s) {
+  if (variant < 0)  // measured best per depth (profiles/kbench_r01.md)
+    variant = BT <= 2 ? 3 : BT == 3 ? 1 : 0;
+  switch (variant) {
+    case 0: return launch3_rule<BT, Geo<2, 4, 8, 1, 4>>(a, rule, hold, s);
+    case 2: return launch3_rule<BT, Geo<2, 2, 8, 2, 4>>(a, rule, hold, s);
+    case 3: return launch3_rule<BT, Geo<2, 4, 4, 2, 4>>(a, rule, hold, s);
+    case 4: return launch3_rule<BT, Geo<1, 4, 8, 2, 4>>(a, rule, hold, s);
+    default: return launch3_rule<BT, Geo<2, 2, 16, 1, 4>>(a, rule, hold, s);
+  }
 }
 
 }  // namespace
@@ -311,29 +358,23 @@ cudaError_t s3d7_advance(const Grid3D& in, const Grid3D& out, int bt, int rule, 
   S3Args a;
   a.in = in.origin;
   a.out = out.origin;
-  a.n = in.n;
+  a.n = int(in.n);
   a.pj_in = in.pitch_j;
   a.pi_in = in.pitch_i;
   a.pj_out = out.pitch_j;
   a.pi_out = out.pitch_i;
-  a.halo = in.halo;
-  a.kout = kKW - 2 * bt;
-  a.jout = kJW - 2 * bt;
-  a.nk = int((a.n + a.kout - 1) / a.kout);
-  a.nj = int((a.n + a.jout - 1) / a.jout);
-  const int64_t tiles = int64_t(a.nk) * a.nj;
-  int64_t want = (2 * 148 * 2 + tiles - 1) / tiles;  // ~2 waves of 2 CTAs/SM
-  int64_t H = (a.n + want - 1) / want;
-  if (H < 8 * bt) H = 8 * bt;
-  if (H > a.n) H = a.n;
-  a.H = int(H);
-  a.nchunks = int((a.n + H - 1) / H);
+  a.halo = int(in.halo);
   a.order = order;
+  static int variant = -2;
+  if (variant == -2) {
+    const char* v = std::getenv("PCOTGPU_S3D7_VARIANT");
+    variant = v ? std::atoi(v) : -1;
+  }
   switch (bt) {
-    case 1: return launch3_bt<1>(a, rule, ring_hold, stream);
-    case 2: return launch3_bt<2>(a, rule, ring_hold, stream);
-    case 3: return launch3_bt<3>(a, rule, ring_hold, stream);
-    default: return launch3_bt<4>(a, rule, ring_hold, stream);
+    case 1: return launch3_bt<1>(a, rule, ring_hold, variant, stream);
+    case 2: return launch3_bt<2>(a, rule, ring_hold, variant, stream);
+    case 3: return launch3_bt<3>(a, rule, ring_hold, variant, stream);
+    default: return launch3_bt<4>(a, rule, ring_hold, variant, stream);
   }
 }
 

@@ -68,7 +68,30 @@ def test_sharded_slabs_equal_single_grid_on_one_gpu():
     assert np.array_equal(split.view(np.uint64), want.view(np.uint64))
 
 
-@pytest.mark.parametrize("variant", [0, 1, 2, 3, 4, 5])
+@pytest.mark.parametrize("variant", [0, 1, 2, 3, 4])
+def test_s3d7_variants_bit_exact(variant):
+    """Every compiled (C, RJ, NW) variant of the 3-D kernel, all depths, both rules."""
+    import subprocess
+    import sys
+
+    code = (
+        "import numpy as np, paper_1802_00166_b200 as P\n"
+        "from tests import oracle_ctypes as O\n"
+        "for k in ('heat3d_b', 'heat3d'):\n"
+        "    want = O.reference_output(k, {'T': 9, 'N': 77})\n"
+        "    with P.GpuExecutor(O.kernel_path(k), {'T': 9, 'N': 77}) as ex:\n"
+        "        for bt in range(1, 5):\n"
+        "            ex.run('slt', [bt, 8, 8, 8], skip_checksum=True)\n"
+        "            out = ex.array_data('Out')\n"
+        "            assert np.array_equal(out.view(np.uint64), want.view(np.uint64)), (k, bt)\n"
+        "print('ok')\n")
+    env = dict(**__import__("os").environ, PCOTGPU_S3D7_VARIANT=str(variant))
+    p = subprocess.run([sys.executable, "-c", code], cwd=O.REPO, env=env, capture_output=True,
+                       text=True, timeout=600)
+    assert p.returncode == 0 and "ok" in p.stdout, p.stdout + p.stderr
+
+
+@pytest.mark.parametrize("variant", [0, 1, 2, 3, 4, 5, 6, 7, 8])
 def test_s2d5_variants_bit_exact(variant, monkeypatch):
     """Every compiled (C, NT, MINB) variant of the 2-D kernel, all depths."""
     import subprocess

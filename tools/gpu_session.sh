@@ -1,9 +1,4 @@
 cd $GRAFT_REPO_ROOT
-timeout 900 python bench.py > gpurun_out/bench3.log 2>&1; echo "bench rc=$?" >> gpurun_out/bench3.log
-timeout 600 python bench.py --steps 2 --warmup 1 > gpurun_out/bench_plain.log 2>&1 && \
-timeout 1200 ncu --metrics gpu__time_duration.sum --clock-control none -c 700 --csv --log-file gpurun_out/launches_r01.csv python bench.py --steps 2 --warmup 1 > gpurun_out/ncu_launches.log 2>&1
-echo "launches rc=$?"
-timeout 600 python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline > gpurun_out/bench_small.log 2>&1 && \
-timeout 1200 ncu --set full --import-source on --clock-control none -k regex:s2d5 -s 90 -c 1 -o gpurun_out/prof_bench_s2d5 python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline > gpurun_out/ncu_full.log 2>&1
-echo "full rc=$?"
-tail -2 gpurun_out/bench3.log
+timeout 900 python -m pytest tests/test_gpu_kernels.py tests/test_gpu_parity.py -q -m gpu -x -k "s3d7 or heat3d or smoke" > gpurun_out/pytest_s3.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_s3.log
+for v in 0 1 2 3 4; do echo "variant $v"; PCOTGPU_S3D7_VARIANT=$v timeout 300 python tools/kbench.py s3d7 --bts 1,2,3,4 2>&1 | grep -v Warn | paste - - ; done > gpurun_out/kb_s3v.log 2>&1
+tail -3 gpurun_out/pytest_s3.log; cat gpurun_out/kb_s3v.log
