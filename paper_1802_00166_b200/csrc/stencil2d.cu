@@ -333,8 +333,12 @@ cudaError_t launch_cfg(S2Args a, int ring_hold, int rows, cudaStream_t stream) {
 // selects another for tuning.
 template <int BT>
 cudaError_t launch_bt(const S2Args& a, int ring_hold, int rows, int variant, cudaStream_t s) {
-  if (variant < 0)  // measured best per depth (tools/kbench.py s2d5; profiles/kbench_r01.md)
-    variant = BT <= 5 ? 6 : BT == 6 ? 5 : 4;
+  if (variant < 0) {  // measured best per depth (tools/kbench.py s2d5; profiles/kbench_r01.md)
+    if (int64_t(rows) * a.cols <= (int64_t(1) << 24))
+      variant = 9;  // small grids: narrow strips so the launch fills 148 SMs
+    else
+      variant = BT <= 5 ? 6 : BT == 6 ? 5 : 4;
+  }
   switch (variant) {
     case 1: return launch_cfg<BT, 2, 256, 2, false>(a, ring_hold, rows, s);
     case 2: return launch_cfg<BT, 4, 256, 1, false>(a, ring_hold, rows, s);
@@ -344,6 +348,8 @@ cudaError_t launch_bt(const S2Args& a, int ring_hold, int rows, int variant, cud
     case 6: return launch_cfg<BT, 4, 128, 4, true>(a, ring_hold, rows, s);
     case 7: return launch_cfg<BT, 2, 256, 2, true>(a, ring_hold, rows, s);
     case 8: return launch_cfg<BT, 2, 128, 4, true>(a, ring_hold, rows, s);
+    case 9: return launch_cfg<BT, 2, 64, 8, true>(a, ring_hold, rows, s);
+    case 10: return launch_cfg<BT, 4, 64, 6, true>(a, ring_hold, rows, s);
     default: return launch_cfg<BT, 4, 128, 2, false>(a, ring_hold, rows, s);
   }
 }
