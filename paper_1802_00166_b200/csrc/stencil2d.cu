@@ -79,10 +79,11 @@ struct EdgeLayout {
   static constexpr int kDoubles = 2 * kPerPar;
 };
 
-template <int BT, int C, int NT, bool MASK, bool HOLD, bool XS, int P>
+template <int BT, int C, int NT, int MASK, bool HOLD, bool XS, int P>
 PCOT_DEV void s2d5_iter(Regs<BT, C>& R, const double* __restrict__ ring_row, int k, int par,
                         double* __restrict__ edge, int warp, int lane, const S2Args& a,
-                        int64_t cb, int r0, int r1, int64_t c0, int64_t cend, bool full_cols) {
+                        int64_t cb, int r0, int r1, int64_t c0, int64_t cend, bool full_cols,
+                        unsigned cmask) {
   constexpr int NW = NT / 32;
   constexpr int SHIFT = 0;  // window start is even for every depth (see s2d5_tile)
   constexpr int EP = EdgeLayout<BT, NT, XS>::kPerPar;
@@ -142,14 +143,18 @@ PCOT_DEV void s2d5_iter(Regs<BT, C>& R, const double* __restrict__ ring_row, int
       s = add(s, right);
       nv[c] = mul(0.2, s);
     }
-    if (MASK) {
-      const int64_t gr = a.g0 + rho;
-      const bool row_in = gr >= 1 && gr <= a.nrows - 2;
+    // MASK bit 1: the strip touches column 0/N-1 -> per-thread column mask;
+    // MASK bit 2: the chunk touches row 0/N-1 -> warp-uniform row test.
+    if (MASK & 1) {
 #pragma unroll
-      for (int c = 0; c < C; ++c) {
-        const int64_t col = cb + c;
-        const bool in = row_in && col >= 1 && col <= a.cols - 2;
-        if (!in) nv[c] = HOLD ? mid[c] : 0.0;
+      for (int c = 0; c < C; ++c)
+        if (!((cmask >> c) & 1u)) nv[c] = HOLD ? mid[c] : 0.0;
+    }
+    if (MASK & 2) {
+      const int64_t gr = a.g0 + rho;
+      if (gr < 1 || gr > a.nrows - 2) {
+#pragma unroll
+        for (int c = 0; c < C; ++c) nv[c] = HOLD ? mid[c] : 0.0;
       }
     }
     if (L + 1 < BT) {
@@ -187,7 +192,7 @@ PCOT_DEV void s2d5_iter(Regs<BT, C>& R, const double* __restrict__ ring_row, int
   }
 }
 
-template <int BT, int C, int NT, bool MASK, bool HOLD, bool XS, int kPF>
+template <int BT, int C, int NT, int MASK, bool HOLD, bool XS, int kPF>
 PCOT_DEV void s2d5_tile(const S2Args& a, int strip, int chunk, double* ring, uint64_t* bars,
                         double* edge) {
   constexpr int W_LOAD = NT * C + 2;
@@ -205,6 +210,10 @@ PCOT_DEV void s2d5_tile(const S2Args& a, int strip, int chunk, double* ring, uin
   const int64_t cs = cfirst;  // even
   const int64_t cb = cfirst + tid * C;
   const bool full_cols = cb >= c0 && cb + C <= cend;
+  unsigned cmask = 0;  // interior columns of this thread
+#pragma unroll
+  for (int c = 0; c < C; ++c)
+    if (cb + c >= 1 && cb + c <= a.cols - 2) cmask |= 1u << c;
 
   auto issue = [&](int64_t it) {
     int64_t row = kstart + it;
@@ -234,7 +243,7 @@ PCOT_DEV void s2d5_tile(const S2Args& a, int strip, int chunk, double* ring, uin
     mbar_wait(&bars[slot], uint32_t((itp / kPF) & 1));                                     \
     s2d5_iter<BT, C, NT, MASK, HOLD, XS, P>(R, ring + slot * W_LOAD, kstart + itp, itp & 1, \
                                             edge, warp, lane, a, cb, r0, r1, c0, cend,      \
-                                            full_cols);                                    \
+                                            full_cols, cmask);                             \
     __syncthreads();                                                                       \
     if (tid == 0 && itp + kPF < niter) issue(itp + kPF);                                   \
   }
@@ -268,13 +277,17 @@ __global__ void __launch_bounds__(NT, MINB) s2d5_kernel(S2Args a) {
   const int64_t c0 = int64_t(strip) * a.w_out - (BT & 1);
   const int64_t r0 = a.row_lo + int64_t(chunk) * a.H;
   const int64_t r1 = r0 + a.H < a.row_hi ? r0 + a.H : a.row_hi;
-  // Tiles whose dependence cone touches the ring (or the outside) need the masked body.
-  const bool edge_tile = (c0 - BT <= 0) || (c0 + a.w_out + BT >= a.cols - 1) ||
-                         (a.g0 + r0 - BT <= 0) || (a.g0 + r1 + BT >= a.nrows - 1);
-  if (edge_tile)
-    s2d5_tile<BT, C, NT, true, HOLD, XS, kPF>(a, strip, chunk, ring, bars, edge);
+  // Tiles whose dependence cone touches the ring (or the outside) need masks:
+  // column-edge strips per element, row-edge chunks by a uniform row test.
+  const bool edge_c = (c0 - BT <= 0) || (c0 + a.w_out + BT >= a.cols - 1);
+  const bool edge_r = (a.g0 + r0 - BT <= 0) || (a.g0 + r1 + BT >= a.nrows - 1);
+  const int mk = (edge_c ? 1 : 0) | (edge_r ? 2 : 0);
+  if (mk == 0)
+    s2d5_tile<BT, C, NT, 0, HOLD, XS, kPF>(a, strip, chunk, ring, bars, edge);
+  else if (mk == 2)
+    s2d5_tile<BT, C, NT, 2, HOLD, XS, kPF>(a, strip, chunk, ring, bars, edge);
   else
-    s2d5_tile<BT, C, NT, false, HOLD, XS, kPF>(a, strip, chunk, ring, bars, edge);
+    s2d5_tile<BT, C, NT, 3, HOLD, XS, kPF>(a, strip, chunk, ring, bars, edge);
 }
 
 // Pick the chunk height so the grid fills whole waves of resident CTAs:
