@@ -61,6 +61,17 @@ __global__ void div9_check_kernel(const double* x, double* q_fast, double* q_ref
   }
 }
 
+// Acquire-spin on a predecessor's completion flag with exponential backoff:
+// thousands of resident warps may be waiting on the wavefront at once, and
+// tight polling would flood L2 with acquire loads.
+PCOT_DEV void spin_flag(const int* f) {
+  unsigned ns = 64;
+  while (ld_acquire(f) == 0) {
+    __nanosleep(ns);
+    ns = ns < 2048 ? ns * 2 : 2048;
+  }
+}
+
 struct GsArgs {
   double* a;
   int64_t ld, n, T;
@@ -87,7 +98,7 @@ __global__ void gs2d_kernel(GsArgs g) {
     if (tid < 8) {
       const int p = g.preds[tile * 8 + tid];
       if (p >= 0)
-        while (ld_acquire(g.flags + p) == 0) __nanosleep(64);
+        spin_flag(g.flags + p);
     }
     __syncthreads();
     const int64_t t0 = 1 + int64_t(tb) * g.bt;
@@ -165,7 +176,7 @@ __global__ void __launch_bounds__(32) gs2d_warp_kernel(GsArgs g) {
     if (lane < 8) {
       const int p = g.preds[tile * 8 + lane];
       if (p >= 0)
-        while (ld_acquire(g.flags + p) == 0) __nanosleep(32);
+        spin_flag(g.flags + p);
     }
     __syncwarp();
     const int t0 = 1 + tb * g.bt;
@@ -173,6 +184,7 @@ __global__ void __launch_bounds__(32) gs2d_warp_kernel(GsArgs g) {
     const int y0 = 4 + yb * g.by;
     const int I0 = x0 - t0 - g.bt;
     const int S0 = y0 - 2 * t0 - 2 * g.bt;
+#pragma unroll 8
     for (int e = lane; e < cells; e += 32) {
       const int r = e / g.ns, c = e - r * g.ns;
       const int i = I0 + r, j = S0 + c - i;
@@ -231,6 +243,170 @@ __global__ void __launch_bounds__(32) gs2d_warp_kernel(GsArgs g) {
   }
 }
 
+// ---------------------------------------------------------------------------
+// Line-group kernel: one warp per tile of 4 time levels x 32 lines (x), each
+// lane owning G = 4 adjacent lines of one time level: lane = tt * 8 + xg,
+// lines x0 + 4*xg + q.  Clock h: line (t, x) processes y = y0 + h - tt -
+// (x - x0), a legal schedule (all dependence distances have positive
+// coordinate sum).  Every value a line needs was produced at clocks h-1..h-4
+// by this lane (own lines q-1, q), by lane-8 (t-1, same lines), lane-1
+// (t, line x-1) or lane-9 (t-1, line x-1): kept in register histories fed by
+// warp shuffles — no block barrier, one __syncwarp per clock for the shared
+// tile region (which holds the halo read by boundary lanes and the values
+// written back at the end).  A point outside the tile/grid contributes its
+// cell's current region value ("virtual output"), which is the right version
+// wherever it is consumed (same UOV argument as the tile schedule).
+namespace lines {
+
+constexpr int BT = 4, G = 4, NXG = 8, BX = G * NXG;  // 4 x 32 lines per warp
+
+struct Hist {
+  double o[G][4];   // own lines, clocks h-1..h-4 (index = clock mod 4)
+  double d[G][4];   // lane-8: (t-1, x_q)
+  double l[4];      // lane-1: (t, x_0 - 1)
+  double dl[4];     // lane-9: (t-1, x_0 - 1)
+};
+
+// Region read with the column guarded: lines far outside their valid clock
+// range index past the region; such values are never consumed.
+PCOT_DEV double rd(const double* reg, int row_base, int col, int ns) {
+  return (col >= 0 && col < ns) ? reg[row_base + col] : 0.0;
+}
+
+template <int P>  // P = h mod 4 (static ring index)
+PCOT_DEV void clock(Hist& H, int h, const GsArgs& g, double* reg, unsigned char* wr,
+                    const int (&pr)[G], const int (&pc)[G], const int (&hlo)[G],
+                    const int (&hhi)[G], int tt, int xg, int ns) {
+  constexpr int M1 = (P + 3) & 3, M2 = (P + 2) & 3, M3 = (P + 1) & 3, M4 = P & 3;
+  // neighbours' outputs of clock h-1
+#pragma unroll
+  for (int q = 0; q < G; ++q) {
+    double v = __shfl_up_sync(0xffffffffu, H.o[q][M1], 8);
+    if (tt == 0) v = rd(reg, pr[q] + ns, pc[q] + h + 2, ns);  // (t0-1, x_q, y_q): halo
+    H.d[q][M1] = v;
+  }
+  {
+    double v = __shfl_up_sync(0xffffffffu, H.o[G - 1][M1], 1);
+    if (xg == 0) v = rd(reg, pr[0] - ns, pc[0] + h, ns);  // (t, x0-1, y_0)
+    H.l[M1] = v;
+    double w = __shfl_up_sync(0xffffffffu, H.o[G - 1][M1], 9);
+    if (tt == 0 || xg == 0) w = rd(reg, pr[0], pc[0] + h + 3, ns);  // (t-1, x0-1, y_0 + 1)
+    H.dl[M1] = w;
+  }
+#pragma unroll
+  for (int q = 0; q < G; ++q) {
+    const int col = pc[q] + h;
+    double out;
+    if (h >= hlo[q] && h < hhi[q]) {
+      const int cell = pr[q] + col;
+      const double a1 = q ? H.o[q - 1][M3] : H.l[M3];
+      const double a2 = q ? H.o[q - 1][M2] : H.l[M2];
+      const double a3 = q ? H.o[q - 1][M1] : H.l[M1];
+      const double c1 = q ? H.d[q - 1][M4] : H.dl[M4];
+      const double c2 = q ? H.d[q - 1][M3] : H.dl[M3];
+      double s = add(a1, a2);
+      s = add(s, a3);
+      s = add(s, H.o[q][M1]);
+      s = add(s, c1);
+      s = add(s, c2);
+      s = add(s, H.d[q][M3]);
+      s = add(s, H.d[q][M2]);
+      s = add(s, H.d[q][M1]);
+      out = div9(s);
+      reg[cell] = out;
+      wr[cell] = 1;
+    } else {
+      out = rd(reg, pr[q], col, ns);
+    }
+    H.o[q][M4] = out;  // becomes "h-1" at the next clock (slot h mod 4)
+  }
+  __syncwarp();
+}
+
+__global__ void __launch_bounds__(32) gs2d_lines_kernel(GsArgs g) {
+  extern __shared__ __align__(16) double reg[];
+  const int cells = g.ni * g.ns;
+  unsigned char* wr = reinterpret_cast<unsigned char*>(reg + cells);
+  const int lane = threadIdx.x;
+  const int tt = lane / NXG, xg = lane - (lane / NXG) * NXG;
+  const int nclk = BT + BX + g.by - 2;
+  for (;;) {
+    int tile = 0;
+    if (lane == 0) tile = atomicAdd(g.counter, 1);
+    tile = __shfl_sync(0xffffffffu, tile, 0);
+    if (tile >= g.ntiles) return;
+    const int tb = g.tiles[tile * 3 + 0], xb = g.tiles[tile * 3 + 1], yb = g.tiles[tile * 3 + 2];
+    if (lane < 8) {
+      const int p = g.preds[tile * 8 + lane];
+      if (p >= 0)
+        spin_flag(g.flags + p);
+    }
+    __syncwarp();
+    const int t0 = 1 + tb * BT, x0 = 2 + xb * BX, y0 = 4 + yb * g.by;
+    const int I0 = x0 - t0 - BT, S0 = y0 - 2 * t0 - 2 * BT;
+#pragma unroll 8
+    for (int e = lane; e < cells; e += 32) {
+      const int r = e / g.ns, c = e - r * g.ns;
+      const int i = I0 + r, j = S0 + c - i;
+      double v = 0.0;
+      if (i >= 0 && i < g.n && j >= 0 && j < g.n) v = ld_cg(g.a + int64_t(i) * g.ld + j);
+      reg[e] = v;
+      wr[e] = 0;
+    }
+    __syncwarp();
+    const int t = t0 + tt;
+    int pr[G], pc[G], hlo[G], hhi[G];
+#pragma unroll
+    for (int q = 0; q < G; ++q) {
+      const int x = x0 + G * xg + q, i = x - t;
+      // y(h) = y0 + h - tt - (x - x0); s = y - 2t; region cell = (i - I0, s - S0)
+      const int yoff = y0 - tt - (x - x0);
+      pr[q] = (i - I0) * g.ns;
+      pc[q] = yoff - 2 * t - S0;  // + h
+      // valid: t <= T, 1 <= i <= n-2, y0 <= y < y0 + by, 1 <= j = y - x - t <= n-2
+      int lo = tt + (x - x0), hi = lo + g.by;
+      const int jlo = 1 + x + t - yoff, jhi = g.n - 2 + x + t - yoff + 1;
+      lo = lo > jlo ? lo : jlo;
+      hi = hi < jhi ? hi : jhi;
+      if (t > g.T || i < 1 || i > g.n - 2) hi = lo;  // empty
+      hlo[q] = lo;
+      hhi[q] = hi;
+    }
+    Hist H;
+    // warm-up clocks -4..-1: every lane is outside the tile, histories fill
+    // with region values (only y >= y0 - 2 entries are ever consumed)
+    int h = -4;
+    clock<0>(H, h, g, reg, wr, pr, pc, hlo, hhi, tt, xg, g.ns);
+    clock<1>(H, h + 1, g, reg, wr, pr, pc, hlo, hhi, tt, xg, g.ns);
+    clock<2>(H, h + 2, g, reg, wr, pr, pc, hlo, hhi, tt, xg, g.ns);
+    clock<3>(H, h + 3, g, reg, wr, pr, pc, hlo, hhi, tt, xg, g.ns);
+    for (h = 0; h < nclk; h += 4) {
+      clock<0>(H, h, g, reg, wr, pr, pc, hlo, hhi, tt, xg, g.ns);
+      clock<1>(H, h + 1, g, reg, wr, pr, pc, hlo, hhi, tt, xg, g.ns);
+      clock<2>(H, h + 2, g, reg, wr, pr, pc, hlo, hhi, tt, xg, g.ns);
+      clock<3>(H, h + 3, g, reg, wr, pr, pc, hlo, hhi, tt, xg, g.ns);
+    }
+    for (int e = lane; e < cells; e += 32) {
+      if (wr[e]) {
+        const int r = e / g.ns, c = e - r * g.ns;
+        const int ii = I0 + r, jj = S0 + c - ii;
+        g.a[int64_t(ii) * g.ld + jj] = reg[e];
+      }
+    }
+    __threadfence();
+    __syncwarp();
+    if (lane == 0) st_release(g.flags + tile, 1);
+  }
+}
+
+}  // namespace lines
+
+// 2: line-group warp kernel (4 x 32 lines), 1: one-warp tile, 0: CTA tile
+int gs_kind(int bt, int bx) {
+  if (bt == lines::BT && bx == lines::BX) return 2;
+  return bt * bx == 32 ? 1 : 0;
+}
+
 }  // namespace
 
 GsPlan* gs2d_plan_create(int64_t n, int64_t T, int bt, int bx, int by, int device) {
@@ -286,12 +462,12 @@ GsPlan* gs2d_plan_create(int64_t n, int64_t T, int bt, int bx, int by, int devic
   cudaMemcpy(p->d_tiles, tiles.data(), tiles.size() * sizeof(int), cudaMemcpyHostToDevice);
   cudaMemcpy(p->d_preds, preds.data(), preds.size() * sizeof(int), cudaMemcpyHostToDevice);
   const int ni = bx + bt + 1, ns = by + 2 * bt + 2;
-  const bool warp = bt * bx == 32;
-  const size_t smem = size_t(ni) * ns * (warp ? 9 : 8) + 16;
-  auto kern = warp ? gs2d_warp_kernel : gs2d_kernel;
+  const int kind = gs_kind(bt, bx);
+  const size_t smem = size_t(ni) * ns * (kind ? 9 : 8) + 16;
+  auto kern = kind == 2 ? lines::gs2d_lines_kernel : kind == 1 ? gs2d_warp_kernel : gs2d_kernel;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
   int occ = 0, sms = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, bt * bx, smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kind ? 32 : bt * bx, smem);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
   p->grid = int(std::max<int64_t>(1, std::min<int64_t>(p->ntiles, int64_t(occ) * sms)));
   return p;
@@ -333,9 +509,11 @@ cudaError_t gs2d_run(GsPlan* p, double* a, int64_t ld, cudaStream_t stream) {
   g.preds = p->d_preds;
   g.flags = p->d_state;
   g.counter = p->d_state + p->ntiles;
-  const bool warp = p->bt * p->bx == 32;
-  const size_t smem = size_t(g.ni) * g.ns * (warp ? 9 : 8) + 16;
-  if (warp)
+  const int kind = gs_kind(p->bt, p->bx);
+  const size_t smem = size_t(g.ni) * g.ns * (kind ? 9 : 8) + 16;
+  if (kind == 2)
+    lines::gs2d_lines_kernel<<<p->grid, 32, smem, stream>>>(g);
+  else if (kind == 1)
     gs2d_warp_kernel<<<p->grid, 32, smem, stream>>>(g);
   else
     gs2d_kernel<<<p->grid, p->bt * p->bx, smem, stream>>>(g);

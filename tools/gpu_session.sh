@@ -1,5 +1,2 @@
 cd $GRAFT_REPO_ROOT
-timeout 900 python -m pytest tests/test_gpu_kernels.py tests/test_gpu_parity.py -q -m gpu -x -k "s2d5 or jacobi or heat2d or sharded or storage or host" > gpurun_out/pytest_s2c.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_s2c.log
-timeout 300 python tools/kbench.py s2d5 --bts 4,5,6,7,8 --orders slt > gpurun_out/kb_auto.log 2>&1
-timeout 600 python bench.py --no-cpu-baseline --no-e2e --steps 3 --warmup 2 2>&1 | tail -1 > gpurun_out/bench4.log
-tail -2 gpurun_out/pytest_s2c.log; cat gpurun_out/kb_auto.log; cut -c1-200 gpurun_out/bench4.log
+timeout 300 python tools/kbench.py gs --tiles 4x32x64 --reps 1 > /dev/null 2>&1 && timeout 900 ncu --set full --import-source on --clock-control none -k regex:lines -s 1 -c 1 -o gpurun_out/prof_gslines python tools/kbench.py gs --tiles 4x32x64 --reps 1 > gpurun_out/ncu_gsl.log 2>&1; echo "ncu rc=$?"
