@@ -234,15 +234,20 @@ struct GpuExecutor::Impl {
     // default tile = best measured (profiles/kbench_r01.md)
     int bt = env_int("PCOTGPU_GS_BT", 2), bx = env_int("PCOTGPU_GS_BX", 64),
         by = env_int("PCOTGPU_GS_BY", 64);
-    if (o.scheme != Scheme::Untiled && o.tile.leaf.size() >= 3) {
+    const bool tiled = o.scheme != Scheme::Untiled && o.tile.leaf.size() >= 3;
+    if (tiled) {
       bt = int(o.tile.leaf[0]);
       bx = int(o.tile.leaf[1]);
       by = int(o.tile.leaf[2]);
     }
-    bt = std::max(1, std::min(bt, 32));
-    bx = std::max(1, std::min(bx, 1024 / bt));
-    by = std::max(2, std::min(by, 2048));
-    while (size_t(bx + bt + 1) * size_t(by + 2 * bt + 2) * 8 > 200 * 1024 && by > 16) by /= 2;
+    if (!tiled && env_int("PCOTGPU_GS_PIPE", 1) && gs2d_pipe_fits(n, T, device)) {
+      bt = bx = by = 0;  // systolic pipeline (one CTA per 32-row band)
+    } else {
+      bt = std::max(1, std::min(bt, 32));
+      bx = std::max(1, std::min(bx, 1024 / bt));
+      by = std::max(2, std::min(by, 2048));
+      while (size_t(bx + bt + 1) * size_t(by + 2 * bt + 2) * 8 > 200 * 1024 && by > 16) by /= 2;
+    }
     if (!gs_plan || gs_cfg[0] != bt || gs_cfg[1] != bx || gs_cfg[2] != by) {
       if (gs_plan) gs2d_plan_destroy(gs_plan);
       gs_plan = gs2d_plan_create(n, T, bt, bx, by, device);

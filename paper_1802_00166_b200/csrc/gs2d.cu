@@ -18,6 +18,8 @@
 // concurrent tile schedule safe for in-place storage.
 // Per point: 3x3 in row-major order, left-associated sum, IEEE '/ 9.0'.
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <map>
 #include <tuple>
 #include <vector>
@@ -36,6 +38,12 @@ struct GsPlan {
   int* d_preds = nullptr;   // [ntiles][8]: predecessor tile ids (-1 = none)
   int* d_state = nullptr;   // [ntiles] flags + [1] queue counter
   int device = 0;
+  // systolic pipeline mode (bt == 0): one CTA per 32-row band
+  bool pipe = false;
+  int nb = 0;
+  int64_t ebld = 0, ld = 0;
+  double* wb[2] = {nullptr, nullptr};
+  double* eb = nullptr;
 };
 
 namespace {
@@ -401,6 +409,313 @@ __global__ void __launch_bounds__(32) gs2d_lines_kernel(GsArgs g) {
 
 }  // namespace lines
 
+// ---------------------------------------------------------------------------
+// Systolic pipeline kernel.  CTA b owns interior rows i0 = 1 + 32b .. i0+31
+// (lane = row) for ALL time levels; its 16 warps hold 16 consecutive time
+// levels at once (warp w handles t = w+1, w+17, ...).  Lane l of a warp at
+// clock c processes column j = c - 2l (row i needs row i-1 two columns
+// ahead: the (t, i-1, j+1) dependence), so a warp sweeps its 32 rows as one
+// skewed wavefront with no barrier at all:
+//   A-terms (t, i-1, j-1..j+1): lane l-1's last three outputs (shuffle);
+//   B (t, i, j-1): own previous output;
+//   C (t-1, i, j..j+1) and D (t-1, i+1, j-1..j+1): the producer warp's
+//   outputs in a 32-column shared-memory ring (one load each per clock,
+//   carried in registers).
+// Warps synchronise per 8-clock chunk through shared-memory progress
+// counters (consumer waits for its producer, producer for its consumer: ring
+// back-pressure); CTAs synchronise through global progress counters per
+// (level, CTA) and exchange their first/last row per level through global
+// edge arrays, prefetched into shared memory with cp.async one chunk ahead.
+// The 16th warp's levels (t = 16, 32, ...) go to a grid-sized global wrap
+// buffer that feeds warp 0's next level (no back-pressure around the ring of
+// warps, so the circular pipeline cannot deadlock).  Level T writes the
+// result in place.  All CTAs must be co-resident (host checks).
+namespace pipe {
+
+// NW warps (= pipelined levels) per CTA, RS-entry producer rings: the ring
+// depth is the slack of the cross-CTA cycle (level t waits on the band below
+// at level t-1, which waits on this band's level t-1, which waits on the ring).
+constexpr int S = 8, IRS = 64, SG = 64;
+constexpr int BIG = 1 << 20;  // progress = level * BIG + completed clocks
+
+struct PipeArgs {
+  double* a;        // in-place grid: F at start, Out at the end
+  double* wb[2];    // wrap-level buffers (grid-shaped, pitch ld)
+  double* eb;       // edge rows [(t * nb + b) * 2 + side][n], kEmpty until written
+  int64_t ld;
+  int64_t ebld;     // edge-row stride (even, >= n + 2)
+  int n, T, nb;
+  int nclk;         // clocks per level (c = -1 .. n + 61)
+  long long* prof;  // optional per-warp cycle counters [nb * NW][8] (PCOTGPU_GS_PROF)
+};
+
+// 16-byte async copy that bypasses L1 (.cg): the sources are written by other
+// warps/CTAs during the kernel, so no stale L1 line may serve them.
+PCOT_DEV void cp16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src));
+}
+
+PCOT_DEV void cp_commit() { asm volatile("cp.async.commit_group;"); }
+PCOT_DEV void cp_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
+PCOT_DEV void cp_wait0() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+
+// CTA-scope acquire/release on the shared-memory progress words: the acquire
+// load is a plain LDS (no fence), the release a CTA membar + STS.
+PCOT_DEV int vld(const volatile int* p) {
+  int v;
+  asm volatile("ld.acquire.cta.shared.s32 %0, [%1];"
+               : "=r"(v)
+               : "r"(smem_u32(const_cast<const int*>(p)))
+               : "memory");
+  return v;
+}
+PCOT_DEV void st_release_cta(volatile int* p, int v) {
+  asm volatile("st.release.cta.shared.s32 [%0], %1;" ::"r"(smem_u32(const_cast<const int*>(p))),
+               "r"(v)
+               : "memory");
+}
+
+// Spins are bounded (~tens of seconds): a scheduling bug then shows up as a
+// wrong result in the parity tests instead of a hung device.
+constexpr long long kSpinCap = 40000000LL;
+
+// Waits are executed by the whole warp (every lane reads the same word, one
+// transaction) and exit on a warp vote: a lane-0-only spin leaves the warp
+// diverged and every later shuffle takes the compiler's slow collective path.
+PCOT_DEV void wait_smem(const volatile int* p, int target) {
+  for (long long it = 0; !__all_sync(0xffffffffu, vld(p) >= target) && it < kSpinCap; ++it)
+    __nanosleep(8);
+}
+
+// Cross-CTA edge values are polled as data: every slot of the edge arrays
+// starts as kEmpty (bytes 0xff, a NaN bit pattern the arithmetic never
+// produces — the device returns the canonical NaN 0x7fff...) and is written
+// exactly once per run, so a non-empty value is final.  No progress counters,
+// no gpu-scope fences: the producer's relaxed store and the consumer's
+// relaxed load of the same 8-byte word are the whole protocol.
+constexpr long long kEmpty = -1LL;
+PCOT_DEV double ld_relaxed(const double* p) {
+  double v;
+  asm volatile("ld.relaxed.gpu.global.f64 %0, [%1];" : "=d"(v) : "l"(p) : "memory");
+  return v;
+}
+PCOT_DEV void st_relaxed(double* p, double v) {
+  asm volatile("st.relaxed.gpu.global.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
+}
+PCOT_DEV bool is_empty(double v) { return __double_as_longlong(v) == kEmpty; }
+
+// Bits kk in [0, 8) with lo <= j0 + kk <= hi.
+PCOT_DEV unsigned span_mask(int j0, int lo, int hi) {
+  const int klo = max(0, lo - j0), khi = min(7, hi - j0);
+  if (klo > khi) return 0u;
+  return ((2u << khi) - 1u) & ~((1u << klo) - 1u);
+}
+
+template <int NW, int RS>
+__global__ void __launch_bounds__(NW * 32, 1) gs2d_pipe_kernel(PipeArgs g) {
+  extern __shared__ __align__(16) double sm[];
+  constexpr int RSP = RS + 1;  // odd lane pitch: ring accesses are bank-conflict free
+  double* rb = sm;                              // [NW][32][RSP] producer rings
+  double* ir = rb + NW * 32 * RSP;              // [32][IRS] warp 0's staged input
+  double* above = ir + 32 * IRS;                // [NW][SG]
+  double* below = above + NW * SG;              // [NW][SG]
+  volatile int* prog = reinterpret_cast<volatile int*>(below + NW * SG);  // [NW]
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, b = blockIdx.x;
+  const int i = 1 + 32 * b + lane;              // this lane's row
+  const int i0 = 1 + 32 * b;
+  const bool row_ok = i <= g.n - 2;
+  const bool has_above = b > 0, has_below = i0 + 32 <= g.n - 2;
+  if (lane == 0) prog[w] = 0;
+  __syncthreads();
+  double* myring = rb + (w * 32 + lane) * RSP;
+  // edge-fetch roles: lanes 0-7 fetch a chunk's eight "above" columns (c+1),
+  // lanes 8-15 its eight "below" columns (c-61)
+  const bool xa = lane < 8, xb = lane >= 8 && lane < 16;
+  double* xring = (xa ? above : below) + w * SG;
+  const double* ab = above + w * SG;
+  const double* be = below + w * SG;
+  long long pacc[7] = {0, 0, 0, 0, 0, 0, 0};
+  for (int t = w + 1; t <= g.T; t += NW) {
+    // producer rows (t-1): warp w-1's ring, or (warp 0) the staged input
+    const double* prow = w ? rb + ((w - 1) * 32 + lane) * RSP : ir + lane * IRS;
+    const double* prow1 = w ? rb + ((w - 1) * 32 + (lane < 31 ? lane + 1 : 31)) * RSP
+                            : ir + (lane < 31 ? lane + 1 : 31) * IRS;
+    const int pmask = w ? RS - 1 : IRS - 1;
+    // (selects, not g.wb[k]: a dynamic index into the parameter struct puts it
+    // in local memory)
+    const double* src0 = (t - 1) == 0 ? g.a : ((((t - 1) / NW) & 1) ? g.wb[1] : g.wb[0]);
+    double* wb_out = ((t / NW) & 1) ? g.wb[1] : g.wb[0];  // warp NW-1 only
+    // edge rows: [(level * nb + cta) * 2 + side] * ebld, side 0 = row i0, 1 = row i0+31
+    const double* eb_above = g.eb + ((int64_t(t) * g.nb + (b - 1)) * 2 + 1) * g.ebld;
+    const double* eb_below = (t - 1) == 0 ? g.a + int64_t(i0 + 32) * g.ld
+                                          : g.eb + ((int64_t(t - 1) * g.nb + (b + 1)) * 2) * g.ebld;
+    double* eb_mine = g.eb + ((int64_t(t) * g.nb + b) * 2) * g.ebld;  // side 0; side 1 at +ebld
+    const double* xrow = xa ? eb_above : eb_below;
+    const bool xlive = xa ? has_above : (xb && has_below);
+    const bool xpoll = xlive && (xa || t > 1);  // level-0 "below" is the input grid
+    const int lvl = t * BIG, plvl = (t - 1) * BIG, clvl = (t + 1) * BIG;
+    const int nchunk = (g.nclk + S - 1) / S;
+    // every producer publishes at most `fin` (its last chunk's clock + 1)
+    const int fin = ((g.nclk + S - 1) / S) * S - 1;
+    auto need = [&](int v) { return v < fin ? v : fin; };
+    auto xcol = [&](int k) { return xa ? k * S + lane : k * S - 62 + (lane - 8); };
+    auto xload = [&](int k) {
+      const int col = xcol(k);
+      double v = 0.0;
+      if (xlive && col >= 0 && col < g.n) v = xpoll ? ld_relaxed(xrow + col) : xrow[col];
+      return v;
+    };
+    // wait until chunk k's edge values are all non-empty, then stage them
+    auto xresolve = [&](int k, double v) {
+      const int col = xcol(k);
+      const bool mine = xpoll && col >= 0 && col < g.n;
+      unsigned ns = 32;
+      for (long long it = 0; __any_sync(0xffffffffu, mine && is_empty(v)) && it < kSpinCap;
+           ++it) {
+        __nanosleep(ns);
+        ns = ns < 256 ? ns * 2 : 256;
+        if (mine && is_empty(v)) v = ld_relaxed(xrow + col);
+      }
+      if ((xa || xb) && col >= 0 && col < g.n) xring[col & (SG - 1)] = v;
+    };
+    // warp 0: rows i0..i0+31 of level t-1, columns [c_lo-2r+1, c_hi-2r+3]
+    auto stage_in = [&](int k) {
+      const int c_lo = k * S - 1, c_hi = (k + 1) * S - 2;
+      const int r = lane;  // one row per lane, 6 pairs each
+      const int row = i0 + r;
+      const int lo = c_lo - 2 * r + 1, hi = c_hi - 2 * r + 3;
+      for (int m = 0; m < 6; ++m) {
+        const int p = (lo & ~1) + 2 * m;
+        if (p <= hi && p >= 0 && p < g.n) {
+          double* dst = ir + r * IRS + (p & (IRS - 1));
+          if (row <= g.n - 1) {
+            cp16(dst, src0 + int64_t(row) * g.ld + p);
+          } else {
+            dst[0] = 0.0;
+            dst[1] = 0.0;
+          }
+        }
+      }
+      cp_commit();
+    };
+    // per-level lane roles of the clock loop
+    const double* dsrc = lane < 31 ? prow1 : be;  // D-term row: lane+1's ring / band below
+    const int dmask = lane < 31 ? pmask : SG - 1;
+    const bool last = t == g.T;
+    const bool wrap_writer = w == NW - 1 && !last && i <= g.n - 1;
+    double* const orow = (last ? g.a : wb_out) + int64_t(i) * g.ld;
+    const bool elane = lane == 0 || lane == 31;  // publish the band's first / last row
+    double* const eside = eb_mine + (lane == 31 ? g.ebld : 0);
+    double a1 = 0, a2 = 0, a3 = 0, c1 = 0, c2 = 0, d1 = 0, d2 = 0, d3 = 0, out = 0;
+    bool staged = false;  // warp 0: chunk k's input already in flight
+    double xv = xload(0);
+    for (int k = 0; k < nchunk; ++k) {
+      const int c_lo = k * S - 1;
+      const int c_hi = c_lo + S - 1;
+      long long tp = g.prof ? clock64() : 0;
+#define PCOT_PROF(slot)                                   \
+  if (g.prof) {                                           \
+    const long long now = clock64();                      \
+    pacc[slot] += now - tp;                               \
+    tp = now;                                             \
+  }
+      // Chunk k's edge values.  Blocking on chunk k (never k+1) before
+      // publishing chunk k keeps the cross-CTA waits acyclic.
+      xresolve(k, xv);
+      if (k + 1 < nchunk) xv = xload(k + 1);  // in flight during this chunk
+      PCOT_PROF(0);
+      bool ahead = false;
+      if (w == 0) {
+        if (!staged) {
+          if (t > 1) wait_smem(prog + NW - 1, plvl + need(c_hi + 5));
+          stage_in(k);
+        }
+        ahead = k + 1 < nchunk &&
+                (t == 1 || __all_sync(0xffffffffu, vld(prog + NW - 1) >= plvl + need(c_hi + S + 5)));
+        if (ahead) stage_in(k + 1);
+        staged = ahead;
+      }
+      PCOT_PROF(1);
+      // intra-CTA producer ahead, consumer not too far behind (ring reuse)
+      if (w > 0) wait_smem(prog + w - 1, plvl + need(c_hi + 5));
+      PCOT_PROF(2);
+      if (w < NW - 1) {
+        // ring reuse: the consumer (level t+1) must have read what this chunk
+        // overwrites; before it starts level t+1 its previous level's reads
+        // (of our level t-NW data) must be over — also when there is no level
+        // t+1, since every slot is written, out-of-range columns included.
+        const int rel = c_hi + 1 - (RS - 4);
+        if (rel > 0) {
+          if (t + 1 <= g.T) wait_smem(prog + w + 1, clvl + need(rel));
+        } else if (t + 1 - NW >= 1) {
+          wait_smem(prog + w + 1, (t + 1 - NW) * BIG + fin);
+        }
+      }
+      PCOT_PROF(3);
+      if (ahead)
+        cp_wait1();  // chunk k landed; chunk k+1 may still be in flight
+      else
+        cp_wait0();
+      __syncwarp();
+      PCOT_PROF(4);
+      // Branch-free clock loop (8 clocks, fully unrolled): per-lane bit masks
+      // over the chunk's clocks replace the per-cell tests, so consecutive
+      // clocks' independent work can overlap the serial sum chain.
+      const int j0 = c_lo - 2 * lane;  // this lane's column at the chunk's first clock
+      const unsigned inb = span_mask(j0, 0, g.n - 1);                 // 0 <= j <= n-1
+      const unsigned upd = row_ok ? span_mask(j0, 1, g.n - 2) : 0u;   // updated cells
+      const unsigned omask = last ? upd : (wrap_writer ? inb : 0u);
+      double* const op = orow + j0;
+      double* const ep = eside + j0;
+      const unsigned emask = elane ? inb : 0u;
+#pragma unroll
+      for (int kk = 0; kk < S; ++kk) {
+        const int q = j0 + kk + 1;
+        const double sh = __shfl_up_sync(0xffffffffu, out, 1);
+        a1 = a2;
+        a2 = a3;
+        a3 = lane ? sh : ab[q & (SG - 1)];
+        c1 = c2;
+        c2 = prow[q & pmask];
+        d1 = d2;
+        d2 = d3;
+        d3 = dsrc[q & dmask];
+        double s = add(a1, a2);
+        s = add(s, a3);
+        s = add(s, out);
+        s = add(s, c1);
+        s = add(s, c2);
+        s = add(s, d1);
+        s = add(s, d2);
+        s = add(s, d3);
+        const double r = div9(s);
+        const double v = (upd >> kk) & 1u ? r : 0.0;
+        out = v;
+        // every column's slot, in range or not: out-of-range slots are only
+        // read by consumer cells that are themselves not updated
+        myring[(j0 + kk) & (RS - 1)] = v;
+        if ((emask >> kk) & 1u) st_relaxed(ep + kk, v);  // lanes 0 / 31: edge rows
+        if ((omask >> kk) & 1u) op[kk] = v;              // result / wrap buffer
+      }
+      PCOT_PROF(5);
+      // publish progress: ring (smem) and wrap-buffer writes are read by other
+      // warps of this CTA only -> CTA-scope release of the counter (lane 0's
+      // release covers the warp's writes through the __syncwarp)
+      __syncwarp();
+      if (lane == 0) st_release_cta(prog + w, lvl + c_hi + 1);
+      __syncwarp();
+      PCOT_PROF(6);
+#undef PCOT_PROF
+    }
+    cp_wait0();
+    __syncwarp();
+  }
+  if (g.prof && lane == 0)
+    for (int q = 0; q < 7; ++q) g.prof[(int64_t(b) * NW + w) * 8 + q] = pacc[q];
+}
+
+}  // namespace pipe
+
 // 2: line-group warp kernel (4 x 32 lines), 1: one-warp tile, 0: CTA tile
 int gs_kind(int bt, int bx) {
   if (bt == lines::BT && bx == lines::BX) return 2;
@@ -418,6 +733,12 @@ GsPlan* gs2d_plan_create(int64_t n, int64_t T, int bt, int bx, int by, int devic
   p->by = by;
   p->device = device;
   if (T < 1 || n < 3) return p;  // nothing to do
+  if (bt == 0) {  // systolic pipeline: every 32-row band's CTA must be resident
+    p->pipe = true;
+    p->nb = int((n - 2 + 31) / 32);
+    p->ebld = (n + 3) & ~int64_t(1);
+    return p;
+  }
   const int64_t NT = (T + bt - 1) / bt;
   const int64_t xmax = T + n - 2, ymax = 2 * T + 2 * (n - 2);
   const int64_t NX = (xmax - 2) / bx + 1, NY = (ymax - 4) / by + 1;
@@ -478,7 +799,112 @@ void gs2d_plan_destroy(GsPlan* p) {
   cudaFree(p->d_tiles);
   cudaFree(p->d_preds);
   cudaFree(p->d_state);
+  cudaFree(p->wb[0]);
+  cudaFree(p->wb[1]);
+  cudaFree(p->eb);
   delete p;
+}
+
+// Pipeline variants: {warps (levels) per CTA, ring depth}.
+struct PipeVariant {
+  int nw, rs;
+  void (*kern)(pipe::PipeArgs);
+};
+const PipeVariant kPipeVariants[] = {
+    {16, 32, pipe::gs2d_pipe_kernel<16, 32>},
+    {12, 64, pipe::gs2d_pipe_kernel<12, 64>},
+    {8, 64, pipe::gs2d_pipe_kernel<8, 64>},
+};
+const PipeVariant& pipe_variant() {
+  const char* s = getenv("PCOTGPU_GS_PIPE_V");
+  const int v = s ? atoi(s) : 1;
+  return kPipeVariants[v < 0 || v > 2 ? 1 : v];
+}
+
+size_t gs2d_pipe_smem(const PipeVariant& v) {
+  using namespace pipe;
+  return size_t(v.nw) * 32 * (v.rs + 1) * 8 + size_t(32) * IRS * 8 + size_t(2) * v.nw * SG * 8 +
+         v.nw * 4;
+}
+
+size_t gs2d_pipe_edge_bytes(int64_t n, int64_t T) {
+  const int64_t nb = (n - 2 + 31) / 32, ebld = (n + 3) & ~int64_t(1);
+  return size_t(T + 1) * nb * 2 * ebld * 8;
+}
+
+// Can the pipeline run n x n for T sweeps?  All bands co-resident (one CTA
+// per SM), progress words level * BIG fit an int, and the write-once edge
+// arrays (16 (T+1) n bytes) stay within a quarter of the free memory.
+bool gs2d_pipe_fits(int64_t n, int64_t T, int device) {
+  if (n < 3 || T < 1 || T >= (int64_t(1) << 31) / pipe::BIG - 1) return false;
+  size_t free_b = 0, total_b = 0;
+  if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) return false;
+  if (gs2d_pipe_edge_bytes(n, T) > free_b / 4) return false;
+  int sms = 0, occ = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+  const PipeVariant& v = pipe_variant();
+  const size_t smem = gs2d_pipe_smem(v);
+  cudaFuncSetAttribute(v.kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, v.kern, v.nw * 32, smem);
+  return occ >= 1 && (n - 2 + 31) / 32 <= int64_t(occ) * sms;
+}
+
+cudaError_t gs2d_pipe_run(GsPlan* p, double* a, int64_t ld, cudaStream_t stream) {
+  using namespace pipe;
+  cudaError_t e;
+  if (!p->eb || p->ld != ld) {
+    cudaFree(p->wb[0]);
+    cudaFree(p->wb[1]);
+    cudaFree(p->eb);
+    p->ld = ld;
+    for (int q = 0; q < 2; ++q)
+      if ((e = cudaMalloc(&p->wb[q], size_t(p->n) * ld * 8)) != cudaSuccess) return e;
+    if ((e = cudaMalloc(&p->eb, gs2d_pipe_edge_bytes(p->n, p->T))) != cudaSuccess) return e;
+  }
+  // every edge slot back to kEmpty (written once per run)
+  if ((e = cudaMemsetAsync(p->eb, 0xff, gs2d_pipe_edge_bytes(p->n, p->T), stream)) != cudaSuccess)
+    return e;
+  PipeArgs g;
+  g.a = a;
+  g.wb[0] = p->wb[0];
+  g.wb[1] = p->wb[1];
+  g.eb = p->eb;
+  g.ld = ld;
+  g.ebld = p->ebld;
+  g.n = int(p->n);
+  g.T = int(p->T);
+  g.nb = p->nb;
+  g.nclk = int(p->n) + 63;
+  g.prof = nullptr;
+  const PipeVariant& v = pipe_variant();
+  const size_t smem = gs2d_pipe_smem(v);
+  if ((e = cudaFuncSetAttribute(v.kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                int(smem))) != cudaSuccess)
+    return e;
+  const char* pe = getenv("PCOTGPU_GS_PROF");  // development aid: cycle breakdown
+  const size_t np = size_t(p->nb) * v.nw * 8;
+  if (pe && atoi(pe)) {
+    if ((e = cudaMalloc(&g.prof, np * 8)) != cudaSuccess) return e;
+    cudaMemsetAsync(g.prof, 0, np * 8, stream);
+  }
+  v.kern<<<p->nb, v.nw * 32, smem, stream>>>(g);
+  count_launch();
+  if (g.prof) {
+    std::vector<long long> h(np);
+    cudaMemcpyAsync(h.data(), g.prof, np * 8, cudaMemcpyDeviceToHost, stream);
+    cudaStreamSynchronize(stream);
+    cudaFree(g.prof);
+    static const char* names[7] = {"wait_xcta", "ready+ahead", "wait_prod", "wait_ring",
+                                   "cp_wait", "compute", "publish"};
+    double tot[7] = {0}, all = 0;
+    for (size_t q = 0; q < np / 8; ++q)
+      for (int m = 0; m < 7; ++m) tot[m] += double(h[q * 8 + m]), all += double(h[q * 8 + m]);
+    fprintf(stderr, "gs pipe profile (nw=%d rs=%d, %lld warps):", v.nw, v.rs, (long long)(np / 8));
+    for (int m = 0; m < 7; ++m)
+      fprintf(stderr, " %s=%.1f%% (%.0f cyc/warp)", names[m], 100 * tot[m] / all, tot[m] / (np / 8));
+    fprintf(stderr, "\n");
+  }
+  return cudaGetLastError();
 }
 
 int64_t gs2d_plan_tiles(const GsPlan* p) { return p ? p->ntiles : 0; }
@@ -491,6 +917,7 @@ cudaError_t div9_check(const double* x, double* q_fast, double* q_ref, int64_t n
 }
 
 cudaError_t gs2d_run(GsPlan* p, double* a, int64_t ld, cudaStream_t stream) {
+  if (p->pipe) return gs2d_pipe_run(p, a, ld, stream);
   if (p->ntiles == 0) return cudaSuccess;
   cudaError_t e = cudaMemsetAsync(p->d_state, 0, (p->ntiles + 1) * sizeof(int), stream);
   if (e != cudaSuccess) return e;

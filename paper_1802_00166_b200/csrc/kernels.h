@@ -45,7 +45,9 @@ int s3d7_max_bt();
 // In-place Gauss-Seidel 9-point, T sweeps, tile wavefront.  `a` is an N x N
 // row-major array with pitch `ld` (ring cells fixed at their value).
 struct GsPlan;  // host-side tile plan (device buffers owned by the plan)
+// bt == 0 selects the systolic pipeline kernel (requires gs2d_pipe_fits).
 GsPlan* gs2d_plan_create(int64_t n, int64_t T, int bt, int bx, int by, int device);
+bool gs2d_pipe_fits(int64_t n, int64_t T, int device);
 void gs2d_plan_destroy(GsPlan* p);
 cudaError_t gs2d_run(GsPlan* p, double* a, int64_t ld, cudaStream_t stream);
 int64_t gs2d_plan_tiles(const GsPlan* p);

@@ -70,6 +70,35 @@ def test_gs2d_tile_shapes(tile):
         assert ex.run("slt", list(tile)).checksum_hex == want
 
 
+GS_PIPE_SHAPES = [(1, 3), (1, 34), (2, 35), (13, 66), (12, 97), (25, 100), (40, 130), (7, 1000)]
+
+
+@pytest.mark.parametrize("variant", [0, 1, 2])
+@pytest.mark.parametrize("T,N", GS_PIPE_SHAPES)
+def test_gs2d_pipeline_matches_oracle(monkeypatch, variant, T, N):
+    """Systolic pipeline (untiled default): every variant (warps per band x ring
+    depth), level counts around the warp count, partial last bands."""
+    monkeypatch.setenv("PCOTGPU_GS_PIPE_V", str(variant))
+    F = O.init_array("F", N * N)
+    want = O.gs2d9(N, T, F)
+    with P.GpuExecutor("gs2d", {"T": T, "N": N}) as ex:
+        ex.run_untiled()
+        got = ex.array_data("Out")
+    assert np.array_equal(got.view(np.uint64), want.view(np.uint64))
+
+
+@pytest.mark.parametrize("variant", [0, 1, 2])
+@pytest.mark.parametrize("T,N", [(16, 1024), (64, 4096)])
+def test_gs2d_pipeline_goldens_repeated(monkeypatch, variant, T, N):
+    """Reference checksums, three runs in a row on one executor (edge slots
+    are re-armed per run; a scheduling race would show as a flaky checksum)."""
+    monkeypatch.setenv("PCOTGPU_GS_PIPE_V", str(variant))
+    want = _golden("gs2d", T=T, N=N)
+    with P.GpuExecutor("gs2d", {"T": T, "N": N}) as ex:
+        for _ in range(3):
+            assert ex.run_untiled().checksum_hex == want
+
+
 def _gemm_check(out, N, rows=None):
     A = O.init_array("A", N * N)
     B = O.init_array("B", N * N)

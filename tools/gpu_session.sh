@@ -1,2 +1,6 @@
 cd $GRAFT_REPO_ROOT
-timeout 300 python tools/kbench.py gs --tiles 4x32x64 --reps 1 > /dev/null 2>&1 && timeout 900 ncu --set full --import-source on --clock-control none -k regex:lines -s 1 -c 1 -o gpurun_out/prof_gslines python tools/kbench.py gs --tiles 4x32x64 --reps 1 > gpurun_out/ncu_gsl.log 2>&1; echo "ncu rc=$?"
+for r in 1 2 3; do for v in 1 0; do PCOTGPU_GS_PIPE_V=$v timeout 120 python tools/gs_once.py 128 4000 2; done; done
+for cfg in "13 4000" "25 1000" "100 2000" "64 4096"; do for v in 1 0 2; do
+  PCOTGPU_GS_PIPE_V=$v timeout 120 python tools/gs_once.py $cfg 2
+done; done
+timeout 600 python -m pytest tests -m gpu -x -q -k "gs" 2>&1 | tail -3
