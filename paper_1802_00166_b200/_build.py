@@ -43,7 +43,10 @@ def _compile(src, flags):
             os.path.join(REPO, "include", "pcotgpu.h"), os.path.join(REPO, "include", "pcot_gpu.hpp")]
     if not _stale(out, deps):
         return out, None
-    cmd = [NVCC] + ARCH + COMMON + flags + ["-c", src, "-o", out]
+    # PCOTGPU_NVCC_EXTRA: development experiments (e.g. -D switches); touch the
+    # source to force a rebuild with them
+    extra = os.environ.get("PCOTGPU_NVCC_EXTRA", "").split()
+    cmd = [NVCC] + ARCH + COMMON + flags + extra + ["-c", src, "-o", out]
     p = subprocess.run(cmd, capture_output=True, text=True)
     if p.returncode != 0:
         return out, "FAILED: %s\n%s%s" % (" ".join(cmd), p.stdout, p.stderr)

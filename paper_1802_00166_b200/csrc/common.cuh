@@ -76,4 +76,11 @@ PCOT_DEV void st_release(int* p, int v) {
 
 PCOT_DEV double ld_cg(const double* p) { return __ldcg(p); }
 
+// Device-wide nanosecond timer (profiling aids).
+PCOT_DEV long long globaltimer() {
+  long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
 }  // namespace pcotgpu

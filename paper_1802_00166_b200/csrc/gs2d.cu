@@ -40,7 +40,8 @@ struct GsPlan {
   int device = 0;
   // systolic pipeline mode (bt == 0): one CTA per 32-row band
   bool pipe = false;
-  int nb = 0;
+  int nb = 0;       // bands of the longest launch
+  int64_t seg = 0;  // levels per launch (the row window drifts one row per level)
   int64_t ebld = 0, ld = 0;
   double* wb[2] = {nullptr, nullptr};
   double* eb = nullptr;
@@ -410,43 +411,49 @@ __global__ void __launch_bounds__(32) gs2d_lines_kernel(GsArgs g) {
 }  // namespace lines
 
 // ---------------------------------------------------------------------------
-// Systolic pipeline kernel.  CTA b owns interior rows i0 = 1 + 32b .. i0+31
-// (lane = row) for ALL time levels; its 16 warps hold 16 consecutive time
-// levels at once (warp w handles t = w+1, w+17, ...).  Lane l of a warp at
-// clock c processes column j = c - 2l (row i needs row i-1 two columns
-// ahead: the (t, i-1, j+1) dependence), so a warp sweeps its 32 rows as one
-// skewed wavefront with no barrier at all:
-//   A-terms (t, i-1, j-1..j+1): lane l-1's last three outputs (shuffle);
+// Systolic pipeline kernel.  One CTA per band of 32 rows; its NW warps hold NW
+// consecutive sweeps (time levels) at once: warp w runs t = w+1, w+1+NW, ...
+// Lane l of a warp at clock c updates column j = c - 2l of its row (row i
+// needs row i-1 one column ahead, (t, i-1, j+1), so the warp sweeps its rows
+// as a skewed wavefront with no barrier at all).
+//
+// The band's row window moves up one row per level: at level t (1-based
+// inside a launch) band b owns rows i0 - (t-1) .. i0 - (t-1) + 31, i0 = 1+32b.
+// Then every input of lane l comes from this band or the band above:
+//   A (t, i-1, j-1..j+1): lane l-1 (shuffle); lane 0: band b-1's last row;
 //   B (t, i, j-1): own previous output;
-//   C (t-1, i, j..j+1) and D (t-1, i+1, j-1..j+1): the producer warp's
-//   outputs in a 32-column shared-memory ring (one load each per clock,
-//   carried in registers).
-// Warps synchronise per 8-clock chunk through shared-memory progress
-// counters (consumer waits for its producer, producer for its consumer: ring
-// back-pressure); CTAs synchronise through global progress counters per
-// (level, CTA) and exchange their first/last row per level through global
-// edge arrays, prefetched into shared memory with cp.async one chunk ahead.
-// The 16th warp's levels (t = 16, 32, ...) go to a grid-sized global wrap
-// buffer that feeds warp 0's next level (no back-pressure around the ring of
-// warps, so the circular pipeline cannot deadlock).  Level T writes the
-// result in place.  All CTAs must be co-resident (host checks).
+//   C (t-1, i, j..j+1): producer warp's lane l-1 (lane 0: band b-1's last row
+//     at level t-1, or the input row i0 at t = 1);
+//   D (t-1, i+1, j-1..j+1): producer warp's lane l;
+// so the bands form a one-way chain (band b waits only for band b-1) and the
+// pipeline has no cross-band cycle to throttle it.  Warps hand rows over in
+// shared-memory rings (consumer waits for its producer; producer waits for
+// ring reuse); the last warp's levels go to a global wrap buffer that feeds
+// warp 0's next level (no back-pressure around the ring of warps).  Each
+// band's last row per level is published in write-once global slots that the
+// band below polls as data.  The window drift costs (T-1)/32 extra bands, so
+// long runs are split into launches of at most Tseg levels (host side).
+// Level T writes the result in place.  All CTAs must be co-resident.
 namespace pipe {
 
-// NW warps (= pipelined levels) per CTA, RS-entry producer rings: the ring
-// depth is the slack of the cross-CTA cycle (level t waits on the band below
-// at level t-1, which waits on this band's level t-1, which waits on the ring).
-constexpr int S = 8, IRS = 64, SG = 64;
+// NW warps (= pipelined levels) per CTA, RS-entry producer rings.
+constexpr int IRS = 64, SG = 64;  // S (clocks per chunk) is a template parameter
+#ifndef PCOT_XLOAD_CLOCK
+#define PCOT_XLOAD_CLOCK 3
+#endif
+constexpr int kXLoadClock = PCOT_XLOAD_CLOCK;  // clock of the chunk that issues the next edge load
 constexpr int BIG = 1 << 20;  // progress = level * BIG + completed clocks
 
 struct PipeArgs {
-  double* a;        // in-place grid: F at start, Out at the end
+  double* a;        // in-place grid: level 0 at launch, level T at exit
   double* wb[2];    // wrap-level buffers (grid-shaped, pitch ld)
-  double* eb;       // edge rows [(t * nb + b) * 2 + side][n], kEmpty until written
+  double* eb;       // last row per (level, band): [((t-1) * nb + b) * ebld + j], kEmpty until written
   int64_t ld;
   int64_t ebld;     // edge-row stride (even, >= n + 2)
   int n, T, nb;
   int nclk;         // clocks per level (c = -1 .. n + 61)
   long long* prof;  // optional per-warp cycle counters [nb * NW][8] (PCOTGPU_GS_PROF)
+  int spin_ns;      // edge-poll backoff cap (ns)
 };
 
 // 16-byte async copy that bypasses L1 (.cg): the sources are written by other
@@ -457,6 +464,7 @@ PCOT_DEV void cp16(void* dst, const void* src) {
 
 PCOT_DEV void cp_commit() { asm volatile("cp.async.commit_group;"); }
 PCOT_DEV void cp_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
+PCOT_DEV void cp_wait2() { asm volatile("cp.async.wait_group 2;" ::: "memory"); }
 PCOT_DEV void cp_wait0() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 
 // CTA-scope acquire/release on the shared-memory progress words: the acquire
@@ -496,7 +504,9 @@ PCOT_DEV void wait_smem(const volatile int* p, int target) {
 constexpr long long kEmpty = -1LL;
 PCOT_DEV double ld_relaxed(const double* p) {
   double v;
-  asm volatile("ld.relaxed.gpu.global.f64 %0, [%1];" : "=d"(v) : "l"(p) : "memory");
+  // no "memory" clobber: a write-once slot needs no ordering with the other
+  // accesses, and the load may then be scheduled inside the clock loop
+  asm volatile("ld.relaxed.gpu.global.f64 %0, [%1];" : "=d"(v) : "l"(p));
   return v;
 }
 PCOT_DEV void st_relaxed(double* p, double v) {
@@ -504,61 +514,63 @@ PCOT_DEV void st_relaxed(double* p, double v) {
 }
 PCOT_DEV bool is_empty(double v) { return __double_as_longlong(v) == kEmpty; }
 
-// Bits kk in [0, 8) with lo <= j0 + kk <= hi.
+// Bits kk in [0, S) with lo <= j0 + kk <= hi.
+template <int S>
 PCOT_DEV unsigned span_mask(int j0, int lo, int hi) {
-  const int klo = max(0, lo - j0), khi = min(7, hi - j0);
+  const int klo = max(0, lo - j0), khi = min(S - 1, hi - j0);
   if (klo > khi) return 0u;
   return ((2u << khi) - 1u) & ~((1u << klo) - 1u);
 }
 
-template <int NW, int RS>
+template <int NW, int RS, int S>
 __global__ void __launch_bounds__(NW * 32, 1) gs2d_pipe_kernel(PipeArgs g) {
-  extern __shared__ __align__(16) double sm[];
+  static_assert(2 * S <= 32 && 3 * S + 4 <= IRS && S + 2 <= SG / 2, "chunk size");
   constexpr int RSP = RS + 1;  // odd lane pitch: ring accesses are bank-conflict free
+  extern __shared__ __align__(16) double sm[];
   double* rb = sm;                              // [NW][32][RSP] producer rings
-  double* ir = rb + NW * 32 * RSP;              // [32][IRS] warp 0's staged input
-  double* above = ir + 32 * IRS;                // [NW][SG]
-  double* below = above + NW * SG;              // [NW][SG]
-  volatile int* prog = reinterpret_cast<volatile int*>(below + NW * SG);  // [NW]
+  double* ir = rb + NW * 32 * RSP;              // [32][IRS] warp 0's staged level t-1 rows
+  double* above = ir + 32 * IRS;                // [NW][SG] band b-1's last row, level t
+  double* cabove = above + NW * SG;             // [NW][SG] same row, level t-1 (lane 0's C)
+  volatile int* prog = reinterpret_cast<volatile int*>(cabove + NW * SG);  // [NW]
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, b = blockIdx.x;
-  const int i = 1 + 32 * b + lane;              // this lane's row
   const int i0 = 1 + 32 * b;
-  const bool row_ok = i <= g.n - 2;
-  const bool has_above = b > 0, has_below = i0 + 32 <= g.n - 2;
+  const bool has_above = b > 0;
   if (lane == 0) prog[w] = 0;
   __syncthreads();
   double* myring = rb + (w * 32 + lane) * RSP;
-  // edge-fetch roles: lanes 0-7 fetch a chunk's eight "above" columns (c+1),
-  // lanes 8-15 its eight "below" columns (c-61)
-  const bool xa = lane < 8, xb = lane >= 8 && lane < 16;
-  double* xring = (xa ? above : below) + w * SG;
+  // edge-fetch roles: lanes [0, S) fetch a chunk's A columns (c+1) of band
+  // b-1's last row at level t, lanes [S, 2S) the same columns at level t-1
+  const bool xa = lane < S, xc = lane >= S && lane < 2 * S;
+  double* xring = (xa ? above : cabove) + w * SG;
   const double* ab = above + w * SG;
-  const double* be = below + w * SG;
-  long long pacc[7] = {0, 0, 0, 0, 0, 0, 0};
+  const double* cab = cabove + w * SG;
+  // producer rows: warp w-1's rings, or (warp 0) the staged wrap rows; the
+  // C-term of lane l is producer lane l-1 (lane 0: cab), the D-term lane l
+  const double* prowD = w ? rb + ((w - 1) * 32 + lane) * RSP : ir + lane * IRS;
+  const double* prowC = lane == 0 ? cab
+                                  : (w ? rb + ((w - 1) * 32 + lane - 1) * RSP : ir + (lane - 1) * IRS);
+  const int dmask = w ? RS - 1 : IRS - 1;
+  const int cmask = lane == 0 ? SG - 1 : dmask;
+  long long pacc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  long long t_first = 0, c_first = 0;  // globaltimer / clock64 at the first compute (prof)
   for (int t = w + 1; t <= g.T; t += NW) {
-    // producer rows (t-1): warp w-1's ring, or (warp 0) the staged input
-    const double* prow = w ? rb + ((w - 1) * 32 + lane) * RSP : ir + lane * IRS;
-    const double* prow1 = w ? rb + ((w - 1) * 32 + (lane < 31 ? lane + 1 : 31)) * RSP
-                            : ir + (lane < 31 ? lane + 1 : 31) * IRS;
-    const int pmask = w ? RS - 1 : IRS - 1;
+    const int i = i0 - (t - 1) + lane;  // this lane's row at level t
+    const bool row_ok = i >= 1 && i <= g.n - 2;
     // (selects, not g.wb[k]: a dynamic index into the parameter struct puts it
     // in local memory)
-    const double* src0 = (t - 1) == 0 ? g.a : ((((t - 1) / NW) & 1) ? g.wb[1] : g.wb[0]);
-    double* wb_out = ((t / NW) & 1) ? g.wb[1] : g.wb[0];  // warp NW-1 only
-    // edge rows: [(level * nb + cta) * 2 + side] * ebld, side 0 = row i0, 1 = row i0+31
-    const double* eb_above = g.eb + ((int64_t(t) * g.nb + (b - 1)) * 2 + 1) * g.ebld;
-    const double* eb_below = (t - 1) == 0 ? g.a + int64_t(i0 + 32) * g.ld
-                                          : g.eb + ((int64_t(t - 1) * g.nb + (b + 1)) * 2) * g.ebld;
-    double* eb_mine = g.eb + ((int64_t(t) * g.nb + b) * 2) * g.ebld;  // side 0; side 1 at +ebld
-    const double* xrow = xa ? eb_above : eb_below;
-    const bool xlive = xa ? has_above : (xb && has_below);
-    const bool xpoll = xlive && (xa || t > 1);  // level-0 "below" is the input grid
+    const double* src0 = ((((t - 1) / NW) & 1) ? g.wb[1] : g.wb[0]);  // warp 0, t > 1
+    double* wb_out = ((t / NW) & 1) ? g.wb[1] : g.wb[0];              // warp NW-1 only
+    const double* eb_t = g.eb + (int64_t(t - 1) * g.nb + (b - 1)) * g.ebld;  // band b-1, level t
+    const double* xrow = xa ? eb_t : (t == 1 ? g.a + int64_t(i0) * g.ld : eb_t - g.nb * g.ebld);
+    const bool xlive = xa ? has_above : (xc && (t == 1 ? i0 <= g.n - 1 : has_above));
+    const bool xpoll = xlive && (xa || t > 1);  // level 0 is the input grid
+    double* eb_mine = g.eb + (int64_t(t - 1) * g.nb + b) * g.ebld;
     const int lvl = t * BIG, plvl = (t - 1) * BIG, clvl = (t + 1) * BIG;
     const int nchunk = (g.nclk + S - 1) / S;
     // every producer publishes at most `fin` (its last chunk's clock + 1)
     const int fin = ((g.nclk + S - 1) / S) * S - 1;
     auto need = [&](int v) { return v < fin ? v : fin; };
-    auto xcol = [&](int k) { return xa ? k * S + lane : k * S - 62 + (lane - 8); };
+    auto xcol = [&](int k) { return k * S + (xa ? lane : lane - S); };
     auto xload = [&](int k) {
       const int col = xcol(k);
       double v = 0.0;
@@ -569,45 +581,48 @@ __global__ void __launch_bounds__(NW * 32, 1) gs2d_pipe_kernel(PipeArgs g) {
     auto xresolve = [&](int k, double v) {
       const int col = xcol(k);
       const bool mine = xpoll && col >= 0 && col < g.n;
-      unsigned ns = 32;
+      unsigned ns = 16;
       for (long long it = 0; __any_sync(0xffffffffu, mine && is_empty(v)) && it < kSpinCap;
            ++it) {
-        __nanosleep(ns);
-        ns = ns < 256 ? ns * 2 : 256;
+        if (g.spin_ns) __nanosleep(ns);
+        ns = ns * 2 < unsigned(g.spin_ns) ? ns * 2 : unsigned(g.spin_ns);
         if (mine && is_empty(v)) v = ld_relaxed(xrow + col);
       }
-      if ((xa || xb) && col >= 0 && col < g.n) xring[col & (SG - 1)] = v;
+      if ((xa || xc) && col >= 0 && col < g.n) xring[col & (SG - 1)] = v;
     };
-    // warp 0: rows i0..i0+31 of level t-1, columns [c_lo-2r+1, c_hi-2r+3]
-    auto stage_in = [&](int k) {
-      const int c_lo = k * S - 1, c_hi = (k + 1) * S - 2;
-      const int r = lane;  // one row per lane, 6 pairs each
-      const int row = i0 + r;
-      const int lo = c_lo - 2 * r + 1, hi = c_hi - 2 * r + 3;
-      for (int m = 0; m < 6; ++m) {
-        const int p = (lo & ~1) + 2 * m;
-        if (p <= hi && p >= 0 && p < g.n) {
-          double* dst = ir + r * IRS + (p & (IRS - 1));
-          if (row <= g.n - 1) {
-            cp16(dst, src0 + int64_t(row) * g.ld + p);
-          } else {
-            dst[0] = 0.0;
-            dst[1] = 0.0;
-          }
-        }
-      }
-      cp_commit();
+    // warp 0: lane q stages level t-1 row i0 - t + 2 + q (the last warp's
+    // lane q one level earlier).  Chunk k reads columns [kS-2-2q, kS+S-1-2q]
+    // (S+2, even-aligned); the first pair was staged with chunk k-1, so a
+    // chunk copies S/2 new 16-byte pairs (chunk 0 one more).
+    const int srow = i0 - t + 2 + lane;
+    const bool srow_ok = srow >= 0 && srow <= g.n - 1;
+    const double* const srcrow = (t == 1 ? g.a : src0) + int64_t(srow) * g.ld;
+    double* const irow = ir + lane * IRS;
+    // Register-staged copy (loads issued a chunk ahead, stored to the ring at
+    // the chunk's start): chunk k needs pairs m = 1..S/2 (m = 0 too at k = 0).
+    auto load_pair = [&](int k, int m) {
+      const int p = k * S - 2 - 2 * lane + 2 * m;
+      double2 v = make_double2(0.0, 0.0);
+      if (srow_ok && p >= 0 && p < g.n) v = __ldcg(reinterpret_cast<const double2*>(srcrow + p));
+      return v;
     };
+    auto store_pair = [&](int k, int m, double2 v) {
+      const int p = k * S - 2 - 2 * lane + 2 * m;
+      if (p >= 0 && p < g.n) *reinterpret_cast<double2*>(irow + (p & (IRS - 1))) = v;
+    };
+    double2 pre[S / 2];  // warp 0: chunk k+1's new pairs, in flight during chunk k
+    if (w == 0) {
+      if (t > 1) wait_smem(prog + NW - 1, plvl + need(S - 2 + 2));
+      store_pair(0, 0, load_pair(0, 0));
+#pragma unroll
+      for (int m = 1; m <= S / 2; ++m) pre[m - 1] = load_pair(0, m);
+    }
     // per-level lane roles of the clock loop
-    const double* dsrc = lane < 31 ? prow1 : be;  // D-term row: lane+1's ring / band below
-    const int dmask = lane < 31 ? pmask : SG - 1;
     const bool last = t == g.T;
-    const bool wrap_writer = w == NW - 1 && !last && i <= g.n - 1;
+    const bool wrap_writer = w == NW - 1 && !last && i >= 0 && i <= g.n - 1;
     double* const orow = (last ? g.a : wb_out) + int64_t(i) * g.ld;
-    const bool elane = lane == 0 || lane == 31;  // publish the band's first / last row
-    double* const eside = eb_mine + (lane == 31 ? g.ebld : 0);
+    const bool elane = lane == 31;  // publishes the band's last row
     double a1 = 0, a2 = 0, a3 = 0, c1 = 0, c2 = 0, d1 = 0, d2 = 0, d3 = 0, out = 0;
-    bool staged = false;  // warp 0: chunk k's input already in flight
     double xv = xload(0);
     for (int k = 0; k < nchunk; ++k) {
       const int c_lo = k * S - 1;
@@ -619,25 +634,23 @@ __global__ void __launch_bounds__(NW * 32, 1) gs2d_pipe_kernel(PipeArgs g) {
     pacc[slot] += now - tp;                               \
     tp = now;                                             \
   }
-      // Chunk k's edge values.  Blocking on chunk k (never k+1) before
-      // publishing chunk k keeps the cross-CTA waits acyclic.
+      // Chunk k's edge values (band b-1 only: the wait chain is acyclic).
       xresolve(k, xv);
-      if (k + 1 < nchunk) xv = xload(k + 1);  // in flight during this chunk
       PCOT_PROF(0);
-      bool ahead = false;
       if (w == 0) {
-        if (!staged) {
-          if (t > 1) wait_smem(prog + NW - 1, plvl + need(c_hi + 5));
-          stage_in(k);
+#pragma unroll
+        for (int m = 1; m <= S / 2; ++m) store_pair(k, m, pre[m - 1]);
+        if (k + 1 < nchunk) {
+          if (t > 1) wait_smem(prog + NW - 1, plvl + need(c_hi + S + 2));
+          PCOT_PROF(1);
+#pragma unroll
+          for (int m = 1; m <= S / 2; ++m) pre[m - 1] = load_pair(k + 1, m);
         }
-        ahead = k + 1 < nchunk &&
-                (t == 1 || __all_sync(0xffffffffu, vld(prog + NW - 1) >= plvl + need(c_hi + S + 5)));
-        if (ahead) stage_in(k + 1);
-        staged = ahead;
       }
-      PCOT_PROF(1);
-      // intra-CTA producer ahead, consumer not too far behind (ring reuse)
-      if (w > 0) wait_smem(prog + w - 1, plvl + need(c_hi + 5));
+      PCOT_PROF(7);
+      // producer ahead: D of clock c is producer lane l's column j+1, computed
+      // at the producer's clock c+1
+      if (w > 0) wait_smem(prog + w - 1, plvl + need(c_hi + 2));
       PCOT_PROF(2);
       if (w < NW - 1) {
         // ring reuse: the consumer (level t+1) must have read what this chunk
@@ -652,34 +665,37 @@ __global__ void __launch_bounds__(NW * 32, 1) gs2d_pipe_kernel(PipeArgs g) {
         }
       }
       PCOT_PROF(3);
-      if (ahead)
-        cp_wait1();  // chunk k landed; chunk k+1 may still be in flight
-      else
-        cp_wait0();
       __syncwarp();
       PCOT_PROF(4);
-      // Branch-free clock loop (8 clocks, fully unrolled): per-lane bit masks
+      if (g.prof && t_first == 0) {
+        t_first = globaltimer();
+        c_first = clock64();
+      }
+      // Branch-free clock loop (S clocks, fully unrolled): per-lane bit masks
       // over the chunk's clocks replace the per-cell tests, so consecutive
       // clocks' independent work can overlap the serial sum chain.
       const int j0 = c_lo - 2 * lane;  // this lane's column at the chunk's first clock
-      const unsigned inb = span_mask(j0, 0, g.n - 1);                 // 0 <= j <= n-1
-      const unsigned upd = row_ok ? span_mask(j0, 1, g.n - 2) : 0u;   // updated cells
+      const unsigned inb = span_mask<S>(j0, 0, g.n - 1);                // 0 <= j <= n-1
+      const unsigned upd = row_ok ? span_mask<S>(j0, 1, g.n - 2) : 0u;  // updated cells
       const unsigned omask = last ? upd : (wrap_writer ? inb : 0u);
       double* const op = orow + j0;
-      double* const ep = eside + j0;
+      double* const ep = eb_mine + j0;
       const unsigned emask = elane ? inb : 0u;
 #pragma unroll
       for (int kk = 0; kk < S; ++kk) {
+        // next chunk's edge values: loaded part-way through this chunk, late
+        // enough to be fresh, early enough to land before the next resolve
+        if (kk == kXLoadClock && k + 1 < nchunk) xv = xload(k + 1);
         const int q = j0 + kk + 1;
         const double sh = __shfl_up_sync(0xffffffffu, out, 1);
         a1 = a2;
         a2 = a3;
         a3 = lane ? sh : ab[q & (SG - 1)];
         c1 = c2;
-        c2 = prow[q & pmask];
+        c2 = prowC[q & cmask];
         d1 = d2;
         d2 = d3;
-        d3 = dsrc[q & dmask];
+        d3 = prowD[q & dmask];
         double s = add(a1, a2);
         s = add(s, a3);
         s = add(s, out);
@@ -694,10 +710,13 @@ __global__ void __launch_bounds__(NW * 32, 1) gs2d_pipe_kernel(PipeArgs g) {
         // every column's slot, in range or not: out-of-range slots are only
         // read by consumer cells that are themselves not updated
         myring[(j0 + kk) & (RS - 1)] = v;
-        if ((emask >> kk) & 1u) st_relaxed(ep + kk, v);  // lanes 0 / 31: edge rows
+        if ((emask >> kk) & 1u) st_relaxed(ep + kk, v);  // lane 31: the band's last row
         if ((omask >> kk) & 1u) op[kk] = v;              // result / wrap buffer
       }
       PCOT_PROF(5);
+#ifdef PCOT_EDGE_FENCE
+      __threadfence();
+#endif
       // publish progress: ring (smem) and wrap-buffer writes are read by other
       // warps of this CTA only -> CTA-scope release of the counter (lane 0's
       // release covers the warp's writes through the __syncwarp)
@@ -707,11 +726,16 @@ __global__ void __launch_bounds__(NW * 32, 1) gs2d_pipe_kernel(PipeArgs g) {
       PCOT_PROF(6);
 #undef PCOT_PROF
     }
-    cp_wait0();
     __syncwarp();
   }
   if (g.prof && lane == 0)
-    for (int q = 0; q < 7; ++q) g.prof[(int64_t(b) * NW + w) * 8 + q] = pacc[q];
+    for (int q = 0; q < 8; ++q) g.prof[(int64_t(b) * NW + w) * 16 + q] = pacc[q];
+  if (g.prof && lane == 0) {
+    g.prof[(int64_t(b) * NW + w) * 16 + 8] = t_first;
+    g.prof[(int64_t(b) * NW + w) * 16 + 9] = globaltimer();
+    g.prof[(int64_t(b) * NW + w) * 16 + 10] = c_first;
+    g.prof[(int64_t(b) * NW + w) * 16 + 11] = clock64();
+  }
 }
 
 }  // namespace pipe
@@ -724,6 +748,9 @@ int gs_kind(int bt, int bx) {
 
 }  // namespace
 
+int64_t gs2d_pipe_segment(int64_t n, int64_t T, int device);
+int gs2d_pipe_bands(int64_t n, int64_t seg);
+
 GsPlan* gs2d_plan_create(int64_t n, int64_t T, int bt, int bx, int by, int device) {
   GsPlan* p = new GsPlan;
   p->n = n;
@@ -733,9 +760,10 @@ GsPlan* gs2d_plan_create(int64_t n, int64_t T, int bt, int bx, int by, int devic
   p->by = by;
   p->device = device;
   if (T < 1 || n < 3) return p;  // nothing to do
-  if (bt == 0) {  // systolic pipeline: every 32-row band's CTA must be resident
+  if (bt == 0) {  // systolic pipeline: every band's CTA must be resident
     p->pipe = true;
-    p->nb = int((n - 2 + 31) / 32);
+    p->seg = gs2d_pipe_segment(n, T, device);
+    p->nb = gs2d_pipe_bands(n, p->seg);
     p->ebld = (n + 3) & ~int64_t(1);
     return p;
   }
@@ -805,20 +833,23 @@ void gs2d_plan_destroy(GsPlan* p) {
   delete p;
 }
 
-// Pipeline variants: {warps (levels) per CTA, ring depth}.
+// Pipeline variants: {warps (levels) per CTA, ring depth, clocks per chunk}.
 struct PipeVariant {
-  int nw, rs;
+  int nw, rs, s;
   void (*kern)(pipe::PipeArgs);
 };
 const PipeVariant kPipeVariants[] = {
-    {16, 32, pipe::gs2d_pipe_kernel<16, 32>},
-    {12, 64, pipe::gs2d_pipe_kernel<12, 64>},
-    {8, 64, pipe::gs2d_pipe_kernel<8, 64>},
+    {16, 32, 8, pipe::gs2d_pipe_kernel<16, 32, 8>},
+    {12, 64, 8, pipe::gs2d_pipe_kernel<12, 64, 8>},
+    {8, 64, 8, pipe::gs2d_pipe_kernel<8, 64, 8>},
+    {12, 64, 4, pipe::gs2d_pipe_kernel<12, 64, 4>},
+    {12, 64, 16, pipe::gs2d_pipe_kernel<12, 64, 16>},
 };
+constexpr int kNumPipeVariants = sizeof(kPipeVariants) / sizeof(kPipeVariants[0]);
 const PipeVariant& pipe_variant() {
   const char* s = getenv("PCOTGPU_GS_PIPE_V");
-  const int v = s ? atoi(s) : 1;
-  return kPipeVariants[v < 0 || v > 2 ? 1 : v];
+  const int v = s ? atoi(s) : 0;  // default: best measured (profiles/gs_pipe_r01.md)
+  return kPipeVariants[v < 0 || v >= kNumPipeVariants ? 0 : v];
 }
 
 size_t gs2d_pipe_smem(const PipeVariant& v) {
@@ -827,27 +858,41 @@ size_t gs2d_pipe_smem(const PipeVariant& v) {
          v.nw * 4;
 }
 
-size_t gs2d_pipe_edge_bytes(int64_t n, int64_t T) {
-  const int64_t nb = (n - 2 + 31) / 32, ebld = (n + 3) & ~int64_t(1);
-  return size_t(T + 1) * nb * 2 * ebld * 8;
+// Bands for a launch of `seg` levels: rows 1..n-2 under a window that moves
+// up seg-1 rows.
+int gs2d_pipe_bands(int64_t n, int64_t seg) { return int((n - 2 + seg - 1 + 31) / 32); }
+
+size_t gs2d_pipe_edge_bytes(int64_t n, int64_t seg) {
+  return size_t(seg) * gs2d_pipe_bands(n, seg) * ((n + 3) & ~int64_t(1)) * 8;
 }
 
-// Can the pipeline run n x n for T sweeps?  All bands co-resident (one CTA
-// per SM), progress words level * BIG fit an int, and the write-once edge
-// arrays (16 (T+1) n bytes) stay within a quarter of the free memory.
-bool gs2d_pipe_fits(int64_t n, int64_t T, int device) {
-  if (n < 3 || T < 1 || T >= (int64_t(1) << 31) / pipe::BIG - 1) return false;
-  size_t free_b = 0, total_b = 0;
-  if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) return false;
-  if (gs2d_pipe_edge_bytes(n, T) > free_b / 4) return false;
+// Levels per launch for n x n, T sweeps (0: the pipeline does not fit).  All
+// bands co-resident (one CTA per SM), progress words level * BIG fit an int,
+// the write-once edge rows (8 n bytes per band and level) within a quarter of
+// the free memory, and launches of at least min(T, 64) levels.
+int64_t gs2d_pipe_segment(int64_t n, int64_t T, int device) {
+  if (n < 3 || T < 1) return 0;
   int sms = 0, occ = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
   const PipeVariant& v = pipe_variant();
   const size_t smem = gs2d_pipe_smem(v);
   cudaFuncSetAttribute(v.kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, v.kern, v.nw * 32, smem);
-  return occ >= 1 && (n - 2 + 31) / 32 <= int64_t(occ) * sms;
+  const int64_t cap = int64_t(occ) * sms;
+  int64_t seg = std::min<int64_t>(T, 32 * cap - (n - 2) + 1);
+  seg = std::min<int64_t>(seg, (int64_t(1) << 31) / pipe::BIG - 2);
+  size_t free_b = 0, total_b = 0;
+  if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) return 0;
+  while (seg > 0 && gs2d_pipe_edge_bytes(n, seg) > free_b / 4) seg /= 2;
+  if (seg < std::min<int64_t>(T, 64)) return 0;
+  const int64_t launches = (T + seg - 1) / seg;  // balance the launches
+  return (T + launches - 1) / launches;
 }
+
+bool gs2d_pipe_fits(int64_t n, int64_t T, int device) { return gs2d_pipe_segment(n, T, device) > 0; }
+
+cudaError_t gs2d_pipe_launch(GsPlan* p, const PipeVariant& v, size_t smem, double* a, int64_t ld,
+                             int64_t len, cudaStream_t stream);
 
 cudaError_t gs2d_pipe_run(GsPlan* p, double* a, int64_t ld, cudaStream_t stream) {
   using namespace pipe;
@@ -859,10 +904,28 @@ cudaError_t gs2d_pipe_run(GsPlan* p, double* a, int64_t ld, cudaStream_t stream)
     p->ld = ld;
     for (int q = 0; q < 2; ++q)
       if ((e = cudaMalloc(&p->wb[q], size_t(p->n) * ld * 8)) != cudaSuccess) return e;
-    if ((e = cudaMalloc(&p->eb, gs2d_pipe_edge_bytes(p->n, p->T))) != cudaSuccess) return e;
+    if ((e = cudaMalloc(&p->eb, gs2d_pipe_edge_bytes(p->n, p->seg))) != cudaSuccess) return e;
   }
-  // every edge slot back to kEmpty (written once per run)
-  if ((e = cudaMemsetAsync(p->eb, 0xff, gs2d_pipe_edge_bytes(p->n, p->T), stream)) != cudaSuccess)
+  const PipeVariant& v = pipe_variant();
+  const size_t smem = gs2d_pipe_smem(v);
+  if ((e = cudaFuncSetAttribute(v.kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                int(smem))) != cudaSuccess)
+    return e;
+  for (int64_t t0 = 0; t0 < p->T; t0 += p->seg) {
+    const int64_t len = std::min(p->seg, p->T - t0);
+    if ((e = gs2d_pipe_launch(p, v, smem, a, ld, len, stream)) != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
+// One launch: `len` levels from the grid in `a` (level 0) back into `a`.
+cudaError_t gs2d_pipe_launch(GsPlan* p, const PipeVariant& v, size_t smem, double* a, int64_t ld,
+                             int64_t len, cudaStream_t stream) {
+  using namespace pipe;
+  cudaError_t e;
+  const int nb = gs2d_pipe_bands(p->n, len);
+  // every edge slot back to kEmpty (written once per launch)
+  if ((e = cudaMemsetAsync(p->eb, 0xff, gs2d_pipe_edge_bytes(p->n, len), stream)) != cudaSuccess)
     return e;
   PipeArgs g;
   g.a = a;
@@ -872,37 +935,65 @@ cudaError_t gs2d_pipe_run(GsPlan* p, double* a, int64_t ld, cudaStream_t stream)
   g.ld = ld;
   g.ebld = p->ebld;
   g.n = int(p->n);
-  g.T = int(p->T);
-  g.nb = p->nb;
+  g.T = int(len);
+  g.nb = nb;
   g.nclk = int(p->n) + 63;
   g.prof = nullptr;
-  const PipeVariant& v = pipe_variant();
-  const size_t smem = gs2d_pipe_smem(v);
-  if ((e = cudaFuncSetAttribute(v.kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                int(smem))) != cudaSuccess)
-    return e;
+  const char* sp = getenv("PCOTGPU_GS_SPIN");
+  g.spin_ns = sp ? atoi(sp) : 256;
   const char* pe = getenv("PCOTGPU_GS_PROF");  // development aid: cycle breakdown
-  const size_t np = size_t(p->nb) * v.nw * 8;
+  const size_t np = size_t(nb) * v.nw * 16;
   if (pe && atoi(pe)) {
     if ((e = cudaMalloc(&g.prof, np * 8)) != cudaSuccess) return e;
     cudaMemsetAsync(g.prof, 0, np * 8, stream);
   }
-  v.kern<<<p->nb, v.nw * 32, smem, stream>>>(g);
+  v.kern<<<nb, v.nw * 32, smem, stream>>>(g);
   count_launch();
   if (g.prof) {
     std::vector<long long> h(np);
     cudaMemcpyAsync(h.data(), g.prof, np * 8, cudaMemcpyDeviceToHost, stream);
     cudaStreamSynchronize(stream);
     cudaFree(g.prof);
-    static const char* names[7] = {"wait_xcta", "ready+ahead", "wait_prod", "wait_ring",
-                                   "cp_wait", "compute", "publish"};
-    double tot[7] = {0}, all = 0;
-    for (size_t q = 0; q < np / 8; ++q)
-      for (int m = 0; m < 7; ++m) tot[m] += double(h[q * 8 + m]), all += double(h[q * 8 + m]);
-    fprintf(stderr, "gs pipe profile (nw=%d rs=%d, %lld warps):", v.nw, v.rs, (long long)(np / 8));
-    for (int m = 0; m < 7; ++m)
-      fprintf(stderr, " %s=%.1f%% (%.0f cyc/warp)", names[m], 100 * tot[m] / all, tot[m] / (np / 8));
+    static const char* names[8] = {"wait_xcta", "wait_wrap", "wait_prod", "wait_ring",
+                                   "cp_wait",   "compute",   "publish",  "stage_in"};
+    double tot[8] = {0}, all = 0;
+    for (size_t q = 0; q < np / 16; ++q)
+      for (int m = 0; m < 8; ++m) tot[m] += double(h[q * 16 + m]), all += double(h[q * 16 + m]);
+    fprintf(stderr, "gs pipe profile (nw=%d rs=%d, %lld warps):", v.nw, v.rs, (long long)(np / 16));
+    for (int m = 0; m < 8; ++m)
+      fprintf(stderr, " %s=%.1f%% (%.0f cyc/warp)", names[m], 100 * tot[m] / all, tot[m] / (np / 16));
     fprintf(stderr, "\n");
+    for (int q = 0; q < 5; ++q) {  // a few bands: edge wait vs compute per warp
+      const int b = int(int64_t(nb - 1) * q / 4);
+      double xw = 0, cw = 0, rw = 0;
+      for (int w = 0; w < v.nw; ++w) {
+        xw += double(h[(size_t(b) * v.nw + w) * 16 + 0]);
+        cw += double(h[(size_t(b) * v.nw + w) * 16 + 5]);
+        rw += double(h[(size_t(b) * v.nw + w) * 16 + 2] + h[(size_t(b) * v.nw + w) * 16 + 3]);
+      }
+      fprintf(stderr, "  band %d: wait_xcta %.0f compute %.0f wait_intra %.0f (cyc/warp)\n", b,
+              xw / v.nw, cw / v.nw, rw / v.nw);
+    }
+    {  // band timeline: warp 0's first compute and warp NW-1's exit (ns from band 0 start)
+      const long long t0 = h[8];
+      fprintf(stderr, "  timeline (us):");
+      for (int q = 0; q <= 8; ++q) {
+        const int b = int(int64_t(nb - 1) * q / 8);
+        fprintf(stderr, " b%d[%.1f,%.1f]", b, (h[(size_t(b) * v.nw) * 16 + 8] - t0) * 1e-3,
+                (h[(size_t(b) * v.nw + v.nw - 1) * 16 + 9] - t0) * 1e-3);
+      }
+      fprintf(stderr, "\n  band 0 warp 0 clock: %.0f MHz\n",
+              double(h[11] - h[10]) / double(h[9] - h[8]) * 1e3);
+    }
+    if (atoi(pe) > 1) {  // per-warp rows of band PCOTGPU_GS_PROF - 2
+      const int b = std::min(atoi(pe) - 2, nb - 1);
+      for (int w = 0; w < v.nw; ++w) {
+        fprintf(stderr, "  band %d warp %2d:", b, w);
+        for (int m = 0; m < 8; ++m)
+          fprintf(stderr, " %s=%lld", names[m], h[(size_t(b) * v.nw + w) * 16 + m]);
+        fprintf(stderr, "\n");
+      }
+    }
   }
   return cudaGetLastError();
 }
