@@ -60,6 +60,13 @@ class GpuExecutor {
 
   ExecResult run(const TileOrder& order, const ExecOptions& opts = {});
   ExecResult run_untiled(const ExecOptions& opts = {});
+  // beyond the reference API: `count` independent runs from host memory with
+  // the host<->device copies overlapped with the compute (two copy streams).
+  // host_inputs[k * ninputs + q]: instance k's input q (dense, array_words);
+  // host_outputs[k]: instance k's output.  Pinned host memory keeps the copies
+  // asynchronous.  Inputs of the last instance remain the executor's inputs.
+  ExecResult run_batch(const TileOrder& order, size_t count, const double* const* host_inputs,
+                       double* const* host_outputs, const ExecOptions& opts = {});
   void reset();
   const std::vector<double>& array_data(const std::string& array) const;
   uint64_t array_base(const std::string& array) const;

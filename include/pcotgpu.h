@@ -96,6 +96,18 @@ int pcotgpu_create(const char* kernel_json, const int64_t* params, size_t nparam
 int pcotgpu_run(pcotgpu_handle* h, const pcotgpu_schedule* sched, pcotgpu_result* res);
 /* Executor::run_untiled — exec.hpp:73. */
 int pcotgpu_run_untiled(pcotgpu_handle* h, pcotgpu_result* res);
+/* Beyond the reference: `count` independent runs straight from host memory
+ * (what a caller of Executor::run does around it: set the inputs, run, read
+ * the output — exec.hpp:71-80), with instance k+1's input copies and instance
+ * k-1's output copy overlapped with instance k's compute.
+ * host_inputs[k * ninputs + q] = instance k's input q (dense, array_words
+ * doubles, inputs in kernel-declaration order); host_outputs[k] = instance k's
+ * output.  res->device_ms covers the whole batch (copies included);
+ * res->checksum is the last instance's output checksum.  Use pinned host
+ * memory for asynchronous copies. */
+int pcotgpu_run_batch(pcotgpu_handle* h, const pcotgpu_schedule* sched, size_t count,
+                      const double* const* host_inputs, double* const* host_outputs,
+                      pcotgpu_result* res);
 /* Executor::reset — exec.hpp:75. */
 int pcotgpu_reset(pcotgpu_handle* h);
 /* Executor::array_data — exec.hpp:76 (inputs and outputs; temps live in the

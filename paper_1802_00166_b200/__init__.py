@@ -78,6 +78,8 @@ _SIGS = [
     ("pcotgpu_create", ctypes.c_int, [ctypes.c_char_p, _I64P, ctypes.c_size_t, ctypes.c_int, ctypes.POINTER(ctypes.c_void_p)]),
     ("pcotgpu_run", ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(Schedule), ctypes.POINTER(ExecResult)]),
     ("pcotgpu_run_untiled", ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(ExecResult)]),
+    ("pcotgpu_run_batch", ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(Schedule), ctypes.c_size_t,
+                                         ctypes.POINTER(_DP), ctypes.POINTER(_DP), ctypes.POINTER(ExecResult)]),
     ("pcotgpu_reset", ctypes.c_int, [ctypes.c_void_p]),
     ("pcotgpu_read_array", ctypes.c_int, [ctypes.c_void_p, ctypes.c_char_p, _DP, ctypes.c_size_t]),
     ("pcotgpu_write_array", ctypes.c_int, [ctypes.c_void_p, ctypes.c_char_p, _DP, ctypes.c_size_t]),
@@ -219,7 +221,8 @@ class GpuExecutor:
     def __exit__(self, *a):
         self.close()
 
-    def run(self, scheme="untiled", tile=None, skip_checksum=False):
+    @staticmethod
+    def _schedule(scheme, tile, skip_checksum):
         s = Schedule()
         s.scheme = SCHEMES[scheme] if isinstance(scheme, str) else int(scheme)
         tile = list(tile or [])
@@ -227,8 +230,52 @@ class GpuExecutor:
         for i, v in enumerate(tile[:8]):
             s.leaf[i] = int(v)
         s.flags = SKIP_CHECKSUM if skip_checksum else 0
+        return s
+
+    @property
+    def input_names(self):
+        return [a["name"] for a in self.spec["arrays"] if a.get("kind") == "input"]
+
+    @property
+    def output_name(self):
+        return [a["name"] for a in self.spec["arrays"] if a.get("kind") == "output"][0]
+
+    def run(self, scheme="untiled", tile=None, skip_checksum=False):
+        s = self._schedule(scheme, tile, skip_checksum)
         r = ExecResult()
         _check(lib().pcotgpu_run(self._h, ctypes.byref(s), ctypes.byref(r)))
+        return r
+
+    def run_batch(self, inputs, outputs, scheme="untiled", tile=None, skip_checksum=False):
+        """`len(outputs)` independent runs from host memory, copies overlapped
+        with the compute (pcotgpu_run_batch).  inputs[k] is instance k's input
+        array, or a sequence of them in `input_names` order; outputs[k] receives
+        instance k's output.  All float64, C-contiguous, array_words long
+        (pinned memory, e.g. torch's pin_memory, keeps the copies async)."""
+        names = self.input_names
+        count = len(outputs)
+        if len(inputs) != count:
+            raise PcotError("DimMismatch", "run_batch: %d input sets for %d outputs" % (len(inputs), count))
+        keep = []
+        ins = (_DP * max(1, count * len(names)))()
+        outs = (_DP * max(1, count))()
+        for k in range(count):
+            per = [inputs[k]] if len(names) == 1 and not isinstance(inputs[k], (list, tuple)) else list(inputs[k])
+            if len(per) != len(names):
+                raise PcotError("DimMismatch", "run_batch: instance %d needs inputs %s" % (k, names))
+            for q, a in enumerate(per):
+                if a.dtype != np.float64 or not a.flags.c_contiguous or a.size != self.array_words(names[q]):
+                    raise PcotError("DimMismatch", "run_batch: input %s of instance %d" % (names[q], k))
+                keep.append(a)
+                ins[k * len(names) + q] = a.ctypes.data_as(_DP)
+            o = outputs[k]
+            if (o.dtype != np.float64 or not o.flags.c_contiguous
+                    or o.size != self.array_words(self.output_name)):
+                raise PcotError("DimMismatch", "run_batch: output of instance %d" % k)
+            outs[k] = o.ctypes.data_as(_DP)
+        s = self._schedule(scheme, tile, skip_checksum)
+        r = ExecResult()
+        _check(lib().pcotgpu_run_batch(self._h, ctypes.byref(s), count, ins, outs, ctypes.byref(r)))
         return r
 
     def run_untiled(self, skip_checksum=False):

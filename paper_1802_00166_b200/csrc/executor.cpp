@@ -88,8 +88,16 @@ struct GpuExecutor::Impl {
   int64_t g_ld = 0;
   int result_slot = -1;  // which buffer holds the output after a run (-1: none)
   mutable std::map<std::string, std::vector<double>> mirror;
+  // batched host runs (run_batch): copy streams and device staging
+  cudaStream_t h2d = nullptr, d2h = nullptr;
+  cudaEvent_t e_start = nullptr, e_in = nullptr, e_prev = nullptr, e_out = nullptr, e_free = nullptr;
+  DevBuf stage_in[2], stage_out;
 
   ~Impl() {
+    for (cudaEvent_t e : {e_start, e_in, e_prev, e_out, e_free})
+      if (e) cudaEventDestroy(e);
+    if (h2d) cudaStreamDestroy(h2d);
+    if (d2h) cudaStreamDestroy(d2h);
     if (gs_plan) gs2d_plan_destroy(gs_plan);
     if (ev0) cudaEventDestroy(ev0);
     if (ev1) cudaEventDestroy(ev1);
@@ -336,6 +344,125 @@ struct GpuExecutor::Impl {
     ck(cudaStreamSynchronize(stream), "D2H");
   }
 
+  // ---------------------------------------------------------------- batched host runs
+  // Dense host input q -> device input buffer `dst` (same layout as in[q]).
+  void h2d_input(int q, double* dst, const double* host, cudaStream_t s) const {
+    const uint64_t w = words_of(rec.inputs[q]);
+    if (rec.ndim == 3 || in_ld == n)
+      ck(cudaMemcpyAsync(dst, host, w * 8, cudaMemcpyHostToDevice, s), "H2D");
+    else
+      ck(cudaMemcpy2DAsync(dst, in_ld * 8, host, n * 8, n * 8, n, cudaMemcpyHostToDevice, s), "H2D");
+  }
+
+  // The output of the last run -> dense device buffer (D2D, on `stream`).
+  void output_to_dense(double* dst) const {
+    switch (rec.family) {
+      case Family::Stencil2D5: {
+        const Slab2D& sl = sg[result_slot];
+        ck(cudaMemcpy2DAsync(dst, n * 8, sl.origin, sl.ld * 8, n * 8, n, cudaMemcpyDeviceToDevice, stream),
+           "D2D");
+        break;
+      }
+      case Family::Stencil3D7: {
+        const Grid3D& g = cg[result_slot];
+        cudaMemcpy3DParms p = {};
+        p.srcPtr = make_cudaPitchedPtr(g.origin, size_t(g.pitch_j) * 8, size_t(n) * 8,
+                                       size_t(g.pitch_i / g.pitch_j));
+        p.dstPtr = make_cudaPitchedPtr(dst, size_t(n) * 8, size_t(n) * 8, size_t(n));
+        p.extent = make_cudaExtent(size_t(n) * 8, size_t(n), size_t(n));
+        p.kind = cudaMemcpyDeviceToDevice;
+        ck(cudaMemcpy3DAsync(&p, stream), "D2D");
+        break;
+      }
+      case Family::GaussSeidel2D9:
+        ck(cudaMemcpy2DAsync(dst, n * 8, gsa.p, gs_ld * 8, n * 8, n, cudaMemcpyDeviceToDevice, stream),
+           "D2D");
+        break;
+      case Family::Gemm:
+        ck(cudaMemcpy2DAsync(dst, n * 8, gC.p, g_ld * 8, n * 8, n, cudaMemcpyDeviceToDevice, stream),
+           "D2D");
+        break;
+    }
+  }
+
+  int run_family(const TileOrder& o) {
+    switch (rec.family) {
+      case Family::Stencil2D5: return run_stencil2d(o);
+      case Family::Stencil3D7: return run_stencil3d(o);
+      case Family::GaussSeidel2D9: return run_gs(o);
+      case Family::Gemm: return run_gemm(o);
+    }
+    return 0;
+  }
+
+  // `count` independent runs from host memory.  Instance k's inputs are copied
+  // in on the h2d stream while instance k-1 computes, and its output leaves on
+  // the d2h stream (through a dense device staging buffer) while instance k+1
+  // computes, so the copies overlap the compute in both directions.
+  ExecResult run_batch(const TileOrder& o, size_t count, const double* const* hin,
+                       double* const* hout, const ExecOptions& opts) {
+    if (opts.sink) fail(ErrorKind::Unsupported, "GpuExecutor: trace sinks are not supported on the device");
+    if (count == 0) fail(ErrorKind::Validation, "run_batch: count must be positive");
+    const size_t ni = rec.inputs.size();
+    for (size_t k = 0; k < count; ++k) {
+      if (!hout || !hout[k]) fail(ErrorKind::Validation, "run_batch: null output pointer");
+      for (size_t q = 0; q < ni; ++q)
+        if (!hin || !hin[k * ni + q]) fail(ErrorKind::Validation, "run_batch: null input pointer");
+    }
+    ck(cudaSetDevice(device), "cudaSetDevice");
+    if (!h2d) {
+      ck(cudaStreamCreateWithFlags(&h2d, cudaStreamNonBlocking), "cudaStreamCreate");
+      ck(cudaStreamCreateWithFlags(&d2h, cudaStreamNonBlocking), "cudaStreamCreate");
+      for (cudaEvent_t* e : {&e_start, &e_in, &e_prev, &e_out, &e_free})
+        ck(cudaEventCreateWithFlags(e, cudaEventDisableTiming), "cudaEventCreate");
+    }
+    if (count > 1)
+      for (size_t q = 0; q < ni; ++q)
+        if (!stage_in[q].p) stage_in[q].alloc(in[q].n);
+    if (!stage_out.p) stage_out.alloc(words_of(rec.output));
+    ExecResult r;
+    const uint64_t l0 = launches();
+    const uint64_t ow = words_of(rec.output);
+    ck(cudaEventRecord(ev0, stream), "cudaEventRecord");
+    ck(cudaEventRecord(e_start, stream), "cudaEventRecord");
+    ck(cudaStreamWaitEvent(h2d, e_start, 0), "wait");
+    ck(cudaStreamWaitEvent(d2h, e_start, 0), "wait");
+    for (size_t q = 0; q < ni; ++q) h2d_input(int(q), in[q].p, hin[q], h2d);
+    ck(cudaEventRecord(e_in, h2d), "cudaEventRecord");
+    for (size_t k = 0; k < count; ++k) {
+      ck(cudaStreamWaitEvent(stream, e_in, 0), "wait");  // instance k's inputs landed
+      if (k > 0)
+        for (size_t q = 0; q < ni; ++q) std::swap(in[q].p, stage_in[q].p);
+      ck(cudaEventRecord(e_prev, stream), "cudaEventRecord");  // instance k-1 done with its inputs
+      if (k + 1 < count) {
+        ck(cudaStreamWaitEvent(h2d, e_prev, 0), "wait");
+        for (size_t q = 0; q < ni; ++q)
+          h2d_input(int(q), stage_in[q].p, hin[(k + 1) * ni + q], h2d);
+        ck(cudaEventRecord(e_in, h2d), "cudaEventRecord");
+      }
+      r.bt = run_family(o);
+      ck(cudaStreamWaitEvent(stream, e_free, 0), "wait");  // staging free (previous D2H done)
+      output_to_dense(stage_out.p);
+      ck(cudaEventRecord(e_out, stream), "cudaEventRecord");
+      ck(cudaStreamWaitEvent(d2h, e_out, 0), "wait");
+      ck(cudaMemcpyAsync(hout[k], stage_out.p, ow * 8, cudaMemcpyDeviceToHost, d2h), "D2H");
+      ck(cudaEventRecord(e_free, d2h), "cudaEventRecord");
+    }
+    ck(cudaStreamWaitEvent(stream, e_free, 0), "wait");
+    ck(cudaEventRecord(ev1, stream), "cudaEventRecord");
+    ck(cudaEventSynchronize(ev1), "run_batch");
+    float ms = 0;
+    ck(cudaEventElapsedTime(&ms, ev0, ev1), "cudaEventElapsedTime");
+    r.device_ms = ms;
+    r.launches = launches() - l0;
+    r.points = rec.points;
+    r.reads = rec.reads;
+    r.writes = rec.writes;
+    mirror.clear();
+    if (!opts.skip_checksum) r.checksum = fnv1a(hout[count - 1], ow * sizeof(double));
+    return r;
+  }
+
   int input_slot(const std::string& a) const {
     for (size_t q = 0; q < rec.inputs.size(); ++q)
       if (rec.inputs[q] == a) return int(q);
@@ -395,6 +522,10 @@ ExecResult GpuExecutor::run(const TileOrder& order, const ExecOptions& opts) {
   return impl_->run(order, opts);
 }
 ExecResult GpuExecutor::run_untiled(const ExecOptions& opts) { return impl_->run(TileOrder{}, opts); }
+ExecResult GpuExecutor::run_batch(const TileOrder& order, size_t count, const double* const* host_inputs,
+                                  double* const* host_outputs, const ExecOptions& opts) {
+  return impl_->run_batch(order, count, host_inputs, host_outputs, opts);
+}
 void GpuExecutor::reset() {
   impl_->init_inputs();
   impl_->result_slot = -1;
@@ -578,6 +709,17 @@ int pcotgpu_run(pcotgpu_handle* h, const pcotgpu_schedule* sched, pcotgpu_result
 }
 
 int pcotgpu_run_untiled(pcotgpu_handle* h, pcotgpu_result* res) { return pcotgpu_run(h, nullptr, res); }
+
+int pcotgpu_run_batch(pcotgpu_handle* h, const pcotgpu_schedule* sched, size_t count,
+                      const double* const* host_inputs, double* const* host_outputs,
+                      pcotgpu_result* res) {
+  return guarded([&] {
+    if (!h || !res) fail(ErrorKind::Validation, "null argument");
+    ExecOptions o;
+    o.skip_checksum = sched && (sched->flags & PCOTGPU_SKIP_CHECKSUM);
+    fill_result(h->ex->run_batch(order_of(sched), count, host_inputs, host_outputs, o), res);
+  });
+}
 
 int pcotgpu_reset(pcotgpu_handle* h) {
   return guarded([&] { h->ex->reset(); });

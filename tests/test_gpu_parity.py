@@ -195,3 +195,43 @@ def test_config4_full_size_windows_and_ring():
         ex.run_untiled(skip_checksum=True)
         out2 = ex.array_data("Out").reshape(N, N)
         assert np.array_equal(out2[:64, :64], corner * 2.0)
+
+
+@pytest.mark.parametrize("kernel,params,tile", [
+    ("jacobi2d", {"T": 40, "N": 1000}, ("slt", [5, 64, 256])),
+    ("heat3d_b", {"T": 20, "N": 130}, ("untiled", None)),
+    ("gs2d", {"T": 16, "N": 1024}, ("untiled", None)),
+    ("gemm", {"N": 127}, ("cot", [16, 16, 16])),
+])
+def test_run_batch_equals_single_runs(kernel, params, tile):
+    """pcotgpu_run_batch: every instance's output equals a separate
+    write_array -> run -> array_data sequence, bit for bit."""
+    with P.GpuExecutor(O.kernel_path(kernel), params) as ex:
+        names = ex.input_names
+        base = [ex.array_data(nm) for nm in names]
+        sets = [[b.copy() for b in base], [2.0 * b for b in base], [b[::-1].copy() for b in base]]
+        outs = [np.empty(ex.array_words(ex.output_name)) for _ in sets]
+        r = ex.run_batch([s if len(s) > 1 else s[0] for s in sets], outs, *tile)
+        assert r.launches > 0
+        for s, got in zip(sets, outs):
+            for nm, a in zip(names, s):
+                ex.write_array(nm, a)
+            ex.run(*tile, skip_checksum=True)
+            want = ex.array_data(ex.output_name)
+            assert np.array_equal(got.view(np.uint64), want.view(np.uint64))
+        assert r.checksum == P.fnv1a(outs[-1])
+
+
+def test_run_batch_errors():
+    with P.GpuExecutor("jacobi2d", {"T": 4, "N": 64}) as ex:
+        F = ex.array_data("F")
+        with pytest.raises(P.PcotError) as e:
+            ex.run_batch([], [])
+        assert e.value.kind == "Validation"
+        with pytest.raises(P.PcotError) as e:
+            ex.run_batch([F], [np.empty(10)])
+        assert e.value.kind == "DimMismatch"
+        one = np.empty(64 * 64)
+        ex.run_batch([F], [one])
+        ex.run_untiled()
+        assert np.array_equal(one, ex.array_data("Out"))
