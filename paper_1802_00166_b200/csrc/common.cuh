@@ -63,6 +63,16 @@ PCOT_DEV void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar
       : "memory");
 }
 
+// Tensor TMA: a 3-D box (c0 fastest) of a tensor map -> shared memory, one
+// instruction for the whole box (SASS: UTMALDG).
+PCOT_DEV void tma_load_3d(void* dst, const void* tmap, int c0, int c1, int c2, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, "
+      "%3, %4}], [%5];" ::"r"(smem_u32(dst)),
+      "l"(tmap), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+      : "memory");
+}
+
 // ---------------------------------------------------------------- acquire/release flags
 PCOT_DEV int ld_acquire(const int* p) {
   int v;

@@ -82,8 +82,7 @@ struct EdgeLayout {
 template <int BT, int C, int NT, int MASK, bool HOLD, bool XS, int P>
 PCOT_DEV void s2d5_iter(Regs<BT, C>& R, const double* __restrict__ ring_row, int k, int par,
                         double* __restrict__ edge, int warp, int lane, const S2Args& a,
-                        int64_t cb, int r0, int r1, int64_t c0, int64_t cend, bool full_cols,
-                        unsigned cmask) {
+                        int64_t cb, int r0, int r1, unsigned smask, unsigned cmask) {
   constexpr int NW = NT / 32;
   constexpr int SHIFT = 0;  // window start is even for every depth (see s2d5_tile)
   constexpr int EP = EdgeLayout<BT, NT, XS>::kPerPar;
@@ -165,17 +164,18 @@ PCOT_DEV void s2d5_iter(Regs<BT, C>& R, const double* __restrict__ ring_row, int
         xs_r(ecur, L + 1)[tid + 1] = nv[C - 1];
       }
     } else if (rho >= r0 && rho < r1) {
+      // smask: this thread's output columns.  Halo threads (mask 0) skip the
+      // store without a divergent scalar path; only grid-edge strips have
+      // partially covered threads.
       double* dst = a.out + int64_t(rho) * a.ld_out + cb;
-      if (SHIFT == 0 && C % 2 == 0 && full_cols) {
+      if (SHIFT == 0 && C % 2 == 0 && smask == (1u << C) - 1u) {
 #pragma unroll
         for (int c = 0; c < C; c += 2)
           __stcs(reinterpret_cast<double2*>(dst + c), make_double2(nv[c], nv[c + 1]));
-      } else {
+      } else if (smask != 0u && smask != (1u << C) - 1u) {
 #pragma unroll
-        for (int c = 0; c < C; ++c) {
-          const int64_t col = cb + c;
-          if (col >= c0 && col < cend) __stcs(dst + c, nv[c]);
-        }
+        for (int c = 0; c < C; ++c)
+          if ((smask >> c) & 1u) __stcs(dst + c, nv[c]);
       }
     }
   }
@@ -209,7 +209,10 @@ PCOT_DEV void s2d5_tile(const S2Args& a, int strip, int chunk, double* ring, uin
   const int64_t cfirst = cstrip - BT;
   const int64_t cs = cfirst;  // even
   const int64_t cb = cfirst + tid * C;
-  const bool full_cols = cb >= c0 && cb + C <= cend;
+  unsigned smask = 0;  // columns this thread stores
+#pragma unroll
+  for (int c = 0; c < C; ++c)
+    if (cb + c >= c0 && cb + c < cend) smask |= 1u << c;
   unsigned cmask = 0;  // interior columns of this thread
 #pragma unroll
   for (int c = 0; c < C; ++c)
@@ -242,8 +245,7 @@ PCOT_DEV void s2d5_tile(const S2Args& a, int strip, int chunk, double* ring, uin
     const int slot = itp % kPF;                                                            \
     mbar_wait(&bars[slot], uint32_t((itp / kPF) & 1));                                     \
     s2d5_iter<BT, C, NT, MASK, HOLD, XS, P>(R, ring + slot * W_LOAD, kstart + itp, itp & 1, \
-                                            edge, warp, lane, a, cb, r0, r1, c0, cend,      \
-                                            full_cols, cmask);                             \
+                                            edge, warp, lane, a, cb, r0, r1, smask, cmask); \
     __syncthreads();                                                                       \
     if (tid == 0 && itp + kPF < niter) issue(itp + kPF);                                   \
   }

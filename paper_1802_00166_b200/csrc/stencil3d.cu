@@ -18,6 +18,9 @@
 // warp-uniform branch; only (j,k)-edge tiles pay per-element selects.
 // Per-point order = the kernel body's parse tree (neighbours (i-1),(i+1),
 // (j-1),(j+1),(k-1),(k+1)); explicit _rn intrinsics, no FMA.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include <cstdlib>
 
 #include "common.cuh"
@@ -331,16 +334,419 @@ cudaError_t launch3_rule(const S3Args& a, int rule, int hold, cudaStream_t s) {
   return hold ? launch3<BT, 1, true, G>(a, s) : launch3<BT, 1, false, G>(a, s);
 }
 
+// ---------------------------------------------------------------------------
+// Version 2: level 0 straight from the TMA plane ring.  The input planes
+// rho-1, rho, rho+1 and the j/k halo are all in shared memory, so the first
+// level needs no register window and no neighbour exchange (its 7 operands
+// are vector shared loads); levels 1..BT-1 keep the 3-plane register window
+// with k-neighbours by shuffle and warp-edge rows through shared memory.
+// Windows start at even k (16-B aligned rows, double2 loads/stores), edge
+// arrays are padded so no thread selects between sources, and ring planes
+// (i = 0 / N-1) take a warp-uniform branch instead of per-element selects.
+template <int C_, int RJ_, int NW_, int MINB_, int PF_>
+struct Geo2 {
+  static constexpr int C = C_, RJ = RJ_, NW = NW_, MINB = MINB_, PF = PF_;
+  static constexpr int NT = NW * 32;
+  static constexpr int KW = 32 * C;   // window k columns
+  static constexpr int JW = NW * RJ;  // window j rows
+  static constexpr int KL = KW + 4;   // ring row: columns kfirst-2 .. kfirst+KW+1
+  static constexpr int JL = JW + 2;   // ring rows: jfirst-1 .. jfirst+JW
+  static constexpr int SLOT = (JL * KL + 15) / 16 * 16;  // ring slot (128-B aligned)
+  static_assert(C % 2 == 0, "double2 rows");
+};
+
+template <int BT, class G>
+struct Regs3v2 {
+  double v[BT > 1 ? BT - 1 : 1][3][G::RJ][G::C];  // levels 1..BT-1
+};
+
+// edges per parity: [warp + 1][top=0 / bottom=1][level 1..BT-1][lane][C]
+template <int BT, class G>
+struct Edge3v2 {
+  static constexpr int LV = BT > 1 ? BT - 1 : 1;
+  static constexpr int EW = 2 * LV * 32 * G::C;  // doubles per warp
+  static constexpr int kPerPar = (G::NW + 2) * EW;
+};
+
+template <int BT, int RULE, bool MASKJK, bool HOLD, class G, int P>
+PCOT_DEV void s3v2_iter(Regs3v2<BT, G>& R, const double* __restrict__ ring, int k, int par,
+                        double* __restrict__ edge, int warp, int lane, const S3Args& a,
+                        unsigned jkmask, int i0, int i1, double* __restrict__ obase,
+                        unsigned smask, int jrow0, int j0, int jend) {
+  constexpr int C = G::C, RJ = G::RJ, KL = G::KL, PF = G::PF, SLOT = G::SLOT;
+  constexpr int EW = Edge3v2<BT, G>::EW;
+  // ring slots of input planes k-2, k-1, k; this thread's cell (r, c) of
+  // plane slot s sits at s*SLOT + (warp*RJ + r + 1)*KL + lane*C + c + 2
+  const int tb = (warp * RJ + 1) * KL + lane * C + 2;
+  const double* p0 = ring + (((k - 2) % PF + PF) % PF) * SLOT + tb;
+  const double* p1 = ring + (((k - 1) % PF + PF) % PF) * SLOT + tb;
+  const double* p2 = ring + ((k % PF + PF) % PF) * SLOT + tb;
+  const double* eprev = edge + (par ^ 1) * Edge3v2<BT, G>::kPerPar;
+  double* ecur = edge + par * Edge3v2<BT, G>::kPerPar;
+  // ---- level 0 -> 1, plane k-1
+  {
+    const int rho = k - 1;
+    double nv[RJ][C];
+    double row[RJ + 2][C];  // plane k-1, rows r-1 .. RJ
+#pragma unroll
+    for (int r = 0; r < RJ + 2; ++r)
+#pragma unroll
+      for (int c = 0; c < C; c += 2) {
+        const double2 v = *reinterpret_cast<const double2*>(p1 + (r - 1) * KL + c);
+        row[r][c] = v.x;
+        row[r][c + 1] = v.y;
+      }
+    const bool ringp = rho < 1 || rho > a.n - 2;
+    if (ringp) {
+#pragma unroll
+      for (int r = 0; r < RJ; ++r)
+#pragma unroll
+        for (int c = 0; c < C; ++c) nv[r][c] = HOLD ? row[r + 1][c] : 0.0;
+    } else {
+#pragma unroll
+      for (int r = 0; r < RJ; ++r) {
+        double im[C], ip[C];
+#pragma unroll
+        for (int c = 0; c < C; c += 2) {
+          const double2 u = *reinterpret_cast<const double2*>(p0 + r * KL + c);
+          const double2 w = *reinterpret_cast<const double2*>(p2 + r * KL + c);
+          im[c] = u.x, im[c + 1] = u.y, ip[c] = w.x, ip[c + 1] = w.y;
+        }
+        const double W = p1[r * KL - 1], E = p1[r * KL + C];
+#pragma unroll
+        for (int c = 0; c < C; ++c) {
+          const double km = c > 0 ? row[r + 1][c > 0 ? c - 1 : 0] : W;
+          const double kp = c < C - 1 ? row[r + 1][c < C - 1 ? c + 1 : 0] : E;
+          nv[r][c] = update7<RULE>(row[r + 1][c], im[c], ip[c], row[r][c], row[r + 2][c], km, kp);
+        }
+      }
+      if (MASKJK) {
+#pragma unroll
+        for (int r = 0; r < RJ; ++r)
+#pragma unroll
+          for (int c = 0; c < C; ++c)
+            if (!((jkmask >> (r * C + c)) & 1u)) nv[r][c] = HOLD ? row[r + 1][c] : 0.0;
+      }
+    }
+    if (BT > 1) {
+      constexpr int s = m3(P);  // level 1's newest plane (k-1) -> slot P
+#pragma unroll
+      for (int r = 0; r < RJ; ++r)
+#pragma unroll
+        for (int c = 0; c < C; ++c) R.v[0][s][r][c] = nv[r][c];
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        ecur[(warp + 1) * EW + ((0 * Edge3v2<BT, G>::LV + 0) * 32 + lane) * C + c] = nv[0][c];
+        ecur[(warp + 1) * EW + ((1 * Edge3v2<BT, G>::LV + 0) * 32 + lane) * C + c] = nv[RJ - 1][c];
+      }
+    } else if (rho >= i0 && rho < i1) {
+#pragma unroll
+      for (int r = 0; r < RJ; ++r) {
+        const int j = jrow0 + r;
+        if (j < j0 || j >= jend) continue;
+        double* dst = obase + int64_t(rho) * a.pi_out + int64_t(j) * a.pj_out;
+        if (smask == (1u << C) - 1u) {
+#pragma unroll
+          for (int c = 0; c < C; c += 2)
+            __stcs(reinterpret_cast<double2*>(dst + c), make_double2(nv[r][c], nv[r][c + 1]));
+        } else if (smask != 0u) {  // grid-edge tiles only; halo lanes store nothing
+#pragma unroll
+          for (int c = 0; c < C; ++c)
+            if ((smask >> c) & 1u) __stcs(dst + c, nv[r][c]);
+        }
+      }
+    }
+  }
+  // ---- levels 1..BT-1 (register window; level index L, R.v[L-1])
+#pragma unroll
+  for (int L = 1; L < BT; ++L) {
+    constexpr int LV = Edge3v2<BT, G>::LV;
+    const int sm = m3(P - L), st = m3(P - L - 1), sb = m3(P - L + 1);
+    const int rho = k - L - 1;
+    const double(*mid)[C] = R.v[L - 1][sm];
+    double nv[RJ][C];
+    const bool ringp = rho < 1 || rho > a.n - 2;
+    if (ringp) {
+#pragma unroll
+      for (int r = 0; r < RJ; ++r)
+#pragma unroll
+        for (int c = 0; c < C; ++c) nv[r][c] = HOLD ? mid[r][c] : 0.0;
+    } else {
+      double up[C], dn[C];
+#pragma unroll
+      for (int c = 0; c < C; ++c) {  // padded: warp 0 / NW-1 read pad rows (halo cells)
+        up[c] = eprev[(warp + 0) * EW + ((1 * LV + (L - 1)) * 32 + lane) * C + c];
+        dn[c] = eprev[(warp + 2) * EW + ((0 * LV + (L - 1)) * 32 + lane) * C + c];
+      }
+#pragma unroll
+      for (int r = 0; r < RJ; ++r) {
+        const double W = __shfl_up_sync(0xffffffffu, mid[r][C - 1], 1);
+        const double E = __shfl_down_sync(0xffffffffu, mid[r][0], 1);
+#pragma unroll
+        for (int c = 0; c < C; ++c) {
+          const double jm = r > 0 ? mid[r > 0 ? r - 1 : 0][c] : up[c];
+          const double jp = r < RJ - 1 ? mid[r < RJ - 1 ? r + 1 : 0][c] : dn[c];
+          const double km = c > 0 ? mid[r][c > 0 ? c - 1 : 0] : W;
+          const double kp = c < C - 1 ? mid[r][c < C - 1 ? c + 1 : 0] : E;
+          nv[r][c] = update7<RULE>(mid[r][c], R.v[L - 1][st][r][c], R.v[L - 1][sb][r][c], jm, jp,
+                                   km, kp);
+        }
+      }
+      if (MASKJK) {
+#pragma unroll
+        for (int r = 0; r < RJ; ++r)
+#pragma unroll
+          for (int c = 0; c < C; ++c)
+            if (!((jkmask >> (r * C + c)) & 1u)) nv[r][c] = HOLD ? mid[r][c] : 0.0;
+      }
+    }
+    if (L + 1 < BT) {
+      constexpr int dummy = 0;
+      (void)dummy;
+      const int sn = m3(P - L);  // level L+1's newest plane k-L-1 -> its slot
+#pragma unroll
+      for (int r = 0; r < RJ; ++r)
+#pragma unroll
+        for (int c = 0; c < C; ++c) R.v[L < BT - 1 ? L : 0][sn][r][c] = nv[r][c];
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        ecur[(warp + 1) * EW + ((0 * LV + L) * 32 + lane) * C + c] = nv[0][c];
+        ecur[(warp + 1) * EW + ((1 * LV + L) * 32 + lane) * C + c] = nv[RJ - 1][c];
+      }
+    } else if (rho >= i0 && rho < i1) {
+#pragma unroll
+      for (int r = 0; r < RJ; ++r) {
+        const int j = jrow0 + r;
+        if (j < j0 || j >= jend) continue;
+        double* dst = obase + int64_t(rho) * a.pi_out + int64_t(j) * a.pj_out;
+        if (smask == (1u << C) - 1u) {
+#pragma unroll
+          for (int c = 0; c < C; c += 2)
+            __stcs(reinterpret_cast<double2*>(dst + c), make_double2(nv[r][c], nv[r][c + 1]));
+        } else if (smask != 0u) {  // grid-edge tiles only; halo lanes store nothing
+#pragma unroll
+          for (int c = 0; c < C; ++c)
+            if ((smask >> c) & 1u) __stcs(dst + c, nv[r][c]);
+        }
+      }
+    }
+  }
+}
+
+template <int BT, int RULE, bool MASKJK, bool HOLD, class G>
+PCOT_DEV void s3v2_tile(const S3Args& a, const CUtensorMap* tmap, int tk, int tj, int chunk,
+                        double* ring, uint64_t* bars, double* edge) {
+  constexpr int C = G::C, RJ = G::RJ, JL = G::JL, KL = G::KL, PF = G::PF, SLOT = G::SLOT;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  // windows start at even k: k0 = tk*kout - (BT&1) makes kfirst = k0 - BT even
+  const int k0u = tk * a.kout - (BT & 1), j0 = tj * a.jout;
+  const int k0 = k0u < 0 ? 0 : k0u;
+  const int kend = k0u + a.kout < a.n ? k0u + a.kout : a.n;
+  const int jend = j0 + a.jout < a.n ? j0 + a.jout : a.n;
+  const int i0 = chunk * a.H;
+  const int i1 = i0 + a.H < a.n ? i0 + a.H : a.n;
+  const int kstart = i0 - BT;
+  const int niter = ((i1 + BT - kstart) + 2) / 3 * 3;
+  const int kfirst = k0u - BT, jfirst = j0 - BT;
+  const int kb = kfirst + lane * C;
+  const int jrow0 = jfirst + warp * RJ;
+  unsigned smask = 0;  // columns this thread stores
+#pragma unroll
+  for (int c = 0; c < C; ++c)
+    if (kb + c >= k0 && kb + c < kend) smask |= 1u << c;
+  const int lo = -a.halo, hi = a.n + a.halo - 1;
+  unsigned jkmask = 0;
+#pragma unroll
+  for (int r = 0; r < RJ; ++r)
+#pragma unroll
+    for (int c = 0; c < C; ++c) {
+      const int j = jrow0 + r, kk = kb + c;
+      if (j >= 1 && j <= a.n - 2 && kk >= 1 && kk <= a.n - 2) jkmask |= 1u << (r * C + c);
+    }
+  double* obase = a.out + kb;
+  // plane `pl` into slot pl mod PF: one tensor-TMA box (KL x JL) starting at
+  // (column kfirst-2, row jfirst-1); the map's origin is the halo corner
+  (void)lo;
+  (void)hi;
+  auto issue = [&](int pl) {  // warp 0, lane 0
+    const int slot = ((pl % PF) + PF) % PF;
+    if (lane == 0) {
+      mbar_arrive_expect_tx(&bars[slot], JL * KL * 8);
+      tma_load_3d(ring + slot * SLOT, tmap, kfirst - 2 + a.halo, jfirst - 1 + a.halo, pl + a.halo,
+                  &bars[slot]);
+    }
+  };
+  // prefetch distance PF-2: slot of plane k+PF-2 held plane k-2, last read at k
+  if (warp == 0)
+    for (int it = 0; it < PF - 2 && it < niter; ++it) issue(kstart + it);
+  Regs3v2<BT, G> R;
+#pragma unroll
+  for (int L = 0; L < Edge3v2<BT, G>::LV; ++L)
+#pragma unroll
+    for (int s = 0; s < 3; ++s)
+#pragma unroll
+      for (int r = 0; r < RJ; ++r)
+#pragma unroll
+        for (int c = 0; c < C; ++c) R.v[L][s][r][c] = 0.0;
+  for (int it = 0; it < niter; it += 3) {
+#define PCOT_S3V2_STEP(P)                                                                    \
+  {                                                                                          \
+    const int itp = it + P;                                                                  \
+    const int k = kstart + itp;                                                              \
+    mbar_wait(&bars[((k % PF) + PF) % PF], uint32_t(((itp) / PF) & 1));                      \
+    s3v2_iter<BT, RULE, MASKJK, HOLD, G, P>(R, ring, k, itp & 1, edge, warp, lane, a, jkmask, \
+                                            i0, i1, obase, smask, jrow0, j0, jend);             \
+    __syncthreads();                                                                         \
+    if (warp == 0 && itp + PF - 2 < niter) issue(k + PF - 2);                                \
+  }
+    PCOT_S3V2_STEP(0)
+    PCOT_S3V2_STEP(1)
+    PCOT_S3V2_STEP(2)
+#undef PCOT_S3V2_STEP
+  }
+}
+
+template <int BT, int RULE, bool HOLD, class G>
+__global__ void __launch_bounds__(G::NT, G::MINB)
+    s3d7v2_kernel(S3Args a, const __grid_constant__ CUtensorMap tmap) {
+  extern __shared__ __align__(128) double smem3[];
+  double* ring = smem3;
+  double* edge = ring + G::PF * G::SLOT;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(edge + 2 * Edge3v2<BT, G>::kPerPar);
+  const int ntile = a.nk * a.nj;
+  int tile = blockIdx.x % ntile, chunk = blockIdx.x / ntile;
+  int tk, tj;
+  if (a.order == kOrderLex) {
+    tj = tile / a.nk;
+    tk = tile - tj * a.nk;
+  } else {  // Morton over (tk, tj)
+    int side = 1;
+    while (side < a.nk || side < a.nj) side <<= 1;
+    int x = 0, y = 0, id = blockIdx.x % (side * side);
+    chunk = blockIdx.x / (side * side);
+    for (int b = 0; b < 12; ++b) {
+      x |= ((id >> (2 * b)) & 1) << b;
+      y |= ((id >> (2 * b + 1)) & 1) << b;
+    }
+    tk = x;
+    tj = y;
+    if (tk >= a.nk || tj >= a.nj) return;
+  }
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < G::PF; ++i) mbar_init(&bars[i], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  const int k0 = tk * a.kout - (BT & 1), j0 = tj * a.jout;
+  const bool edge_jk = (k0 - BT <= 0) || (k0 + a.kout + BT >= a.n - 1) || (j0 - BT <= 0) ||
+                       (j0 + a.jout + BT >= a.n - 1);
+  if (edge_jk)
+    s3v2_tile<BT, RULE, true, HOLD, G>(a, &tmap, tk, tj, chunk, ring, bars, edge);
+  else
+    s3v2_tile<BT, RULE, false, HOLD, G>(a, &tmap, tk, tj, chunk, ring, bars, edge);
+}
+
+// 3-D tensor map over the whole padded input cube (halo included), box KL x JL x 1.
+cudaError_t encode_plane_map(CUtensorMap* m, const S3Args& a, int kl, int jl) {
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+  if (!encode) {
+    cudaDriverEntryPointQueryResult q;
+    void* fn = nullptr;
+    cudaError_t e = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q);
+    if (e != cudaSuccess || q != cudaDriverEntryPointSuccess || !fn) return cudaErrorNotSupported;
+    encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  }
+  const double* base = a.in - int64_t(a.halo) * (a.pi_in + a.pj_in + 1);
+  const cuuint64_t dims[3] = {cuuint64_t(a.pj_in), cuuint64_t(a.pi_in / a.pj_in),
+                              cuuint64_t(a.n + 2 * a.halo)};
+  const cuuint64_t strides[2] = {cuuint64_t(a.pj_in) * 8, cuuint64_t(a.pi_in) * 8};
+  const cuuint32_t box[3] = {cuuint32_t(kl), cuuint32_t(jl), 1};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = encode(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(base), dims,
+                      strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
+}
+
+template <int BT, int RULE, bool HOLD, class G>
+cudaError_t launch3v2(S3Args a, cudaStream_t stream) {
+  constexpr size_t smem = size_t(G::PF) * G::SLOT * 8 +
+                          size_t(2) * Edge3v2<BT, G>::kPerPar * 8 + G::PF * 8;
+  auto fn = s3d7v2_kernel<BT, RULE, HOLD, G>;
+  static int slots = 0;
+  if (slots == 0) {
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    if (e != cudaSuccess) return e;
+    int occ = 0, sms = 0, dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, G::NT, smem);
+    slots = (occ > 0 ? occ : 1) * (sms > 0 ? sms : 148);
+  }
+  a.kout = G::KW - 2 * BT;
+  a.jout = G::JW - 2 * BT;
+  a.nk = (a.n + (BT & 1) + a.kout - 1) / a.kout;
+  a.nj = (a.n + a.jout - 1) / a.jout;
+  const int64_t tiles = int64_t(a.nk) * a.nj;
+  int best = 1;
+  double bestc = 1e300;
+  for (int nc = 1; nc <= (a.n / (4 * BT) > 1 ? a.n / (4 * BT) : 1); ++nc) {
+    const int H = (a.n + nc - 1) / nc;
+    const int64_t waves = (tiles * nc + slots - 1) / slots;
+    const double cost = double(waves) * (H + 2 * BT + 2);
+    if (cost < bestc * 0.999) bestc = cost, best = nc;
+  }
+  a.nchunks = best;
+  a.H = (a.n + best - 1) / best;
+  int grid;
+  if (a.order == kOrderLex) {
+    grid = a.nk * a.nj * a.nchunks;
+  } else {
+    int side = 1;
+    while (side < a.nk || side < a.nj) side <<= 1;
+    grid = side * side * a.nchunks;
+  }
+  CUtensorMap tmap;
+  cudaError_t e = encode_plane_map(&tmap, a, G::KL, G::JL);
+  if (e != cudaSuccess) return e;
+  fn<<<grid, G::NT, smem, stream>>>(a, tmap);
+  count_launch();
+  return cudaGetLastError();
+}
+
+template <int BT, class G>
+cudaError_t launch3v2_rule(const S3Args& a, int rule, int hold, cudaStream_t s) {
+  if (rule == 0) return hold ? launch3v2<BT, 0, true, G>(a, s) : launch3v2<BT, 0, false, G>(a, s);
+  return hold ? launch3v2<BT, 1, true, G>(a, s) : launch3v2<BT, 1, false, G>(a, s);
+}
+
 // Variant table (C, RJ, NW, MINB, PF); PCOTGPU_S3D7_VARIANT selects one.
 template <int BT>
 cudaError_t launch3_bt(const S3Args& a, int rule, int hold, int variant, cudaStream_t s) {
-  if (variant < 0)  // measured best per depth (profiles/kbench_r01.md)
-    variant = BT <= 2 ? 3 : BT == 3 ? 1 : 0;
+  if (variant < 0)  // measured best per depth (profiles/s3d7_r01.md)
+    variant = BT == 1 ? 3 : BT == 2 ? 14 : BT == 3 ? 15 : 0;
+  if (variant >= 10 && BT > 3) variant = 0;  // version 2 holds at most 2 register levels
   switch (variant) {
     case 0: return launch3_rule<BT, Geo<2, 4, 8, 1, 4>>(a, rule, hold, s);
     case 2: return launch3_rule<BT, Geo<2, 2, 8, 2, 4>>(a, rule, hold, s);
     case 3: return launch3_rule<BT, Geo<2, 4, 4, 2, 4>>(a, rule, hold, s);
     case 4: return launch3_rule<BT, Geo<1, 4, 8, 2, 4>>(a, rule, hold, s);
+    // version 2 (level 0 from the plane ring), BT <= 3
+    case 10: return launch3v2_rule<BT <= 3 ? BT : 1, Geo2<2, 4, 8, 1, 6>>(a, rule, hold, s);
+    case 11: return launch3v2_rule<BT <= 3 ? BT : 1, Geo2<2, 4, 4, 2, 4>>(a, rule, hold, s);
+    case 12: return launch3v2_rule<BT <= 3 ? BT : 1, Geo2<2, 2, 8, 2, 4>>(a, rule, hold, s);
+    case 13: return launch3v2_rule<BT <= 3 ? BT : 1, Geo2<4, 2, 8, 1, 4>>(a, rule, hold, s);
+    case 14: return launch3v2_rule<BT <= 3 ? BT : 1, Geo2<2, 4, 8, 1, 4>>(a, rule, hold, s);
+    case 15: return launch3v2_rule<BT <= 3 ? BT : 1, Geo2<2, 4, 16, 1, 4>>(a, rule, hold, s);
+    case 16: return launch3v2_rule<BT <= 3 ? BT : 1, Geo2<2, 2, 16, 1, 4>>(a, rule, hold, s);
+    case 17: return launch3v2_rule<BT <= 3 ? BT : 1, Geo2<2, 4, 12, 1, 4>>(a, rule, hold, s);
+    case 18: return launch3v2_rule<BT <= 3 ? BT : 1, Geo2<2, 3, 16, 1, 4>>(a, rule, hold, s);
+    case 19: return launch3v2_rule<BT <= 3 ? BT : 1, Geo2<2, 4, 8, 1, 8>>(a, rule, hold, s);
+    case 20: return launch3v2_rule<BT <= 3 ? BT : 1, Geo2<2, 3, 16, 1, 5>>(a, rule, hold, s);
+    case 21: return launch3v2_rule<BT <= 3 ? BT : 1, Geo2<2, 4, 4, 2, 6>>(a, rule, hold, s);
+    case 22: return launch3v2_rule<BT <= 3 ? BT : 1, Geo2<2, 4, 8, 2, 4>>(a, rule, hold, s);
+    case 23: return launch3v2_rule<BT <= 3 ? BT : 1, Geo2<2, 4, 6, 2, 4>>(a, rule, hold, s);
+    case 24: return launch3v2_rule<BT <= 3 ? BT : 1, Geo2<2, 4, 12, 1, 4>>(a, rule, hold, s);
     default: return launch3_rule<BT, Geo<2, 2, 16, 1, 4>>(a, rule, hold, s);
   }
 }
