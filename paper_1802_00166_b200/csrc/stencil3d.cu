@@ -343,9 +343,10 @@ cudaError_t launch3_rule(const S3Args& a, int rule, int hold, cudaStream_t s) {
 // Windows start at even k (16-B aligned rows, double2 loads/stores), edge
 // arrays are padded so no thread selects between sources, and ring planes
 // (i = 0 / N-1) take a warp-uniform branch instead of per-element selects.
-template <int C_, int RJ_, int NW_, int MINB_, int PF_>
+template <int C_, int RJ_, int NW_, int MINB_, int PF_, bool RC_ = false>
 struct Geo2 {
   static constexpr int C = C_, RJ = RJ_, NW = NW_, MINB = MINB_, PF = PF_;
+  static constexpr bool RC = RC_;     // level-0 rows cached in registers (3 planes)
   static constexpr int NT = NW * 32;
   static constexpr int KW = 32 * C;   // window k columns
   static constexpr int JW = NW * RJ;  // window j rows
@@ -358,6 +359,7 @@ struct Geo2 {
 template <int BT, class G>
 struct Regs3v2 {
   double v[BT > 1 ? BT - 1 : 1][3][G::RJ][G::C];  // levels 1..BT-1
+  double z[G::RC ? 3 : 1][G::RJ][G::C];           // level-0 rows 0..RJ-1 (RC)
 };
 
 // edges per parity: [warp + 1][top=0 / bottom=1][level 1..BT-1][lane][C]
@@ -388,14 +390,36 @@ PCOT_DEV void s3v2_iter(Regs3v2<BT, G>& R, const double* __restrict__ ring, int 
     const int rho = k - 1;
     double nv[RJ][C];
     double row[RJ + 2][C];  // plane k-1, rows r-1 .. RJ
+    if constexpr (G::RC) {
+      // plane k's rows stay in registers for its next two uses (centre, i-1)
 #pragma unroll
-    for (int r = 0; r < RJ + 2; ++r)
+      for (int r = 0; r < RJ; ++r)
+#pragma unroll
+        for (int c = 0; c < C; c += 2) {
+          const double2 v = *reinterpret_cast<const double2*>(p2 + r * KL + c);
+          R.z[G::RC ? m3(P) : 0][r][c] = v.x;
+          R.z[G::RC ? m3(P) : 0][r][c + 1] = v.y;
+        }
+#pragma unroll
+      for (int r = 0; r < RJ; ++r)
+#pragma unroll
+        for (int c = 0; c < C; ++c) row[r + 1][c] = R.z[G::RC ? m3(P - 1) : 0][r][c];
 #pragma unroll
       for (int c = 0; c < C; c += 2) {
-        const double2 v = *reinterpret_cast<const double2*>(p1 + (r - 1) * KL + c);
-        row[r][c] = v.x;
-        row[r][c + 1] = v.y;
+        const double2 u = *reinterpret_cast<const double2*>(p1 - KL + c);
+        const double2 w = *reinterpret_cast<const double2*>(p1 + RJ * KL + c);
+        row[0][c] = u.x, row[0][c + 1] = u.y, row[RJ + 1][c] = w.x, row[RJ + 1][c + 1] = w.y;
       }
+    } else {
+#pragma unroll
+      for (int r = 0; r < RJ + 2; ++r)
+#pragma unroll
+        for (int c = 0; c < C; c += 2) {
+          const double2 v = *reinterpret_cast<const double2*>(p1 + (r - 1) * KL + c);
+          row[r][c] = v.x;
+          row[r][c + 1] = v.y;
+        }
+    }
     const bool ringp = rho < 1 || rho > a.n - 2;
     if (ringp) {
 #pragma unroll
@@ -406,11 +430,19 @@ PCOT_DEV void s3v2_iter(Regs3v2<BT, G>& R, const double* __restrict__ ring, int 
 #pragma unroll
       for (int r = 0; r < RJ; ++r) {
         double im[C], ip[C];
+        if constexpr (G::RC) {
 #pragma unroll
-        for (int c = 0; c < C; c += 2) {
-          const double2 u = *reinterpret_cast<const double2*>(p0 + r * KL + c);
-          const double2 w = *reinterpret_cast<const double2*>(p2 + r * KL + c);
-          im[c] = u.x, im[c + 1] = u.y, ip[c] = w.x, ip[c + 1] = w.y;
+          for (int c = 0; c < C; ++c) {
+            im[c] = R.z[G::RC ? m3(P - 2) : 0][r][c];
+            ip[c] = R.z[G::RC ? m3(P) : 0][r][c];
+          }
+        } else {
+#pragma unroll
+          for (int c = 0; c < C; c += 2) {
+            const double2 u = *reinterpret_cast<const double2*>(p0 + r * KL + c);
+            const double2 w = *reinterpret_cast<const double2*>(p2 + r * KL + c);
+            im[c] = u.x, im[c + 1] = u.y, ip[c] = w.x, ip[c + 1] = w.y;
+          }
         }
         const double W = p1[r * KL - 1], E = p1[r * KL + C];
 #pragma unroll
@@ -420,7 +452,7 @@ PCOT_DEV void s3v2_iter(Regs3v2<BT, G>& R, const double* __restrict__ ring, int 
           nv[r][c] = update7<RULE>(row[r + 1][c], im[c], ip[c], row[r][c], row[r + 2][c], km, kp);
         }
       }
-      if (MASKJK) {
+      if (MASKJK && jkmask != (1u << (RJ * C)) - 1u) {  // only threads with ring cells
 #pragma unroll
         for (int r = 0; r < RJ; ++r)
 #pragma unroll
@@ -492,7 +524,7 @@ PCOT_DEV void s3v2_iter(Regs3v2<BT, G>& R, const double* __restrict__ ring, int 
                                    km, kp);
         }
       }
-      if (MASKJK) {
+      if (MASKJK && jkmask != (1u << (RJ * C)) - 1u) {  // only threads with ring cells
 #pragma unroll
         for (int r = 0; r < RJ; ++r)
 #pragma unroll
@@ -588,6 +620,12 @@ PCOT_DEV void s3v2_tile(const S3Args& a, const CUtensorMap* tmap, int tk, int tj
       for (int r = 0; r < RJ; ++r)
 #pragma unroll
         for (int c = 0; c < C; ++c) R.v[L][s][r][c] = 0.0;
+#pragma unroll
+  for (int s = 0; s < (G::RC ? 3 : 1); ++s)
+#pragma unroll
+    for (int r = 0; r < RJ; ++r)
+#pragma unroll
+      for (int c = 0; c < C; ++c) R.z[s][r][c] = 0.0;
   for (int it = 0; it < niter; it += 3) {
 #define PCOT_S3V2_STEP(P)                                                                    \
   {                                                                                          \
@@ -724,7 +762,7 @@ cudaError_t launch3v2_rule(const S3Args& a, int rule, int hold, cudaStream_t s) 
 template <int BT>
 cudaError_t launch3_bt(const S3Args& a, int rule, int hold, int variant, cudaStream_t s) {
   if (variant < 0)  // measured best per depth (profiles/s3d7_r01.md)
-    variant = BT == 1 ? 3 : BT == 2 ? 14 : BT == 3 ? 15 : 0;
+    variant = BT == 1 ? 29 : BT == 2 ? 28 : BT == 3 ? 15 : 0;
   if (variant >= 10 && BT > 3) variant = 0;  // version 2 holds at most 2 register levels
   switch (variant) {
     case 0: return launch3_rule<BT, Geo<2, 4, 8, 1, 4>>(a, rule, hold, s);
@@ -747,6 +785,13 @@ cudaError_t launch3_bt(const S3Args& a, int rule, int hold, int variant, cudaStr
     case 22: return launch3v2_rule<BT <= 3 ? BT : 1, Geo2<2, 4, 8, 2, 4>>(a, rule, hold, s);
     case 23: return launch3v2_rule<BT <= 3 ? BT : 1, Geo2<2, 4, 6, 2, 4>>(a, rule, hold, s);
     case 24: return launch3v2_rule<BT <= 3 ? BT : 1, Geo2<2, 4, 12, 1, 4>>(a, rule, hold, s);
+    case 25: return launch3v2_rule<BT <= 3 ? BT : 1, Geo2<2, 4, 8, 1, 4, true>>(a, rule, hold, s);
+    case 26: return launch3v2_rule<BT <= 3 ? BT : 1, Geo2<2, 4, 16, 1, 4, true>>(a, rule, hold, s);
+    case 27: return launch3v2_rule<BT <= 3 ? BT : 1, Geo2<2, 4, 8, 2, 4, true>>(a, rule, hold, s);
+    case 28: return launch3v2_rule<BT <= 3 ? BT : 1, Geo2<2, 4, 8, 2, 5, true>>(a, rule, hold, s);
+    case 29: return launch3v2_rule<BT <= 3 ? BT : 1, Geo2<2, 4, 6, 2, 4, true>>(a, rule, hold, s);
+    case 30: return launch3v2_rule<BT <= 3 ? BT : 1, Geo2<2, 3, 8, 2, 4, true>>(a, rule, hold, s);
+    case 31: return launch3v2_rule<BT <= 3 ? BT : 1, Geo2<2, 4, 6, 2, 5, true>>(a, rule, hold, s);
     default: return launch3_rule<BT, Geo<2, 2, 16, 1, 4>>(a, rule, hold, s);
   }
 }

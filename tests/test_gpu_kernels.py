@@ -68,7 +68,7 @@ def test_sharded_slabs_equal_single_grid_on_one_gpu():
     assert np.array_equal(split.view(np.uint64), want.view(np.uint64))
 
 
-@pytest.mark.parametrize("variant", [0, 1, 2, 3, 4, 10, 11, 12, 13, 14, 15, 16, 17, 18, 19, 20, 21, 22, 23, 24])
+@pytest.mark.parametrize("variant", [0, 1, 2, 3, 4, 10, 11, 12, 13, 14, 15, 16, 17, 18, 19, 20, 21, 22, 23, 24, 25, 26, 27, 28, 29, 30, 31])
 def test_s3d7_variants_bit_exact(variant):
     """Every compiled (C, RJ, NW) variant of the 3-D kernel, all depths, both rules."""
     import subprocess
