@@ -32,9 +32,9 @@ REPO = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, REPO)
 
 EMIT_DIR = os.path.join(REPO, "oracle", "_ref", "emit")
-SAMPLE = "jacobi2d_N8192_T32"
+SAMPLE = "jacobi2d_N8192_T160"
 SAMPLE_INIT = "jacobi2d_N8192_T0"
-SAMPLE_UPDATES = 8192 * 8192 * 32
+SAMPLE_UPDATES = 8192 * 8192 * 160
 METRIC = "stencil GUpdates/s"
 
 
@@ -147,7 +147,7 @@ def cpu_baseline_port(threads):
     O.lib().oracle_set_threads(threads)
     F = O.init_array("F", 8192 * 8192)
     t0 = time.perf_counter()
-    O.stencil2d5(8192, 32, 0, F)
+    O.stencil2d5(8192, 160, 0, F)
     return time.perf_counter() - t0
 
 
@@ -165,7 +165,7 @@ def cpu_baseline(threads):
         kind = "port"
     return {"value": SAMPLE_UPDATES / secs / 1e9, "unit": "GUpdates/s", "cores": threads,
             "kind": kind, "seconds": round(secs, 3), "checksum": chk,
-            "sample": "Jacobi-2D 8192^2, T=32 (same rule/ring/init as config 4; "
+            "sample": "Jacobi-2D 8192^2, T=160 (same rule/ring/init as config 4; "
                       "reference emitted recursive C, OpenMP tasks, -O2 -ffp-contract=off; "
                       "wall minus init-only run)"}
 
@@ -190,10 +190,10 @@ def reference_arm(args, rank, world):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (reference init_value)", "impl": "reference",
-        "config": {"workload": "jacobi2d 8192x8192 T=32 (bounded CPU sample of config 4)",
+        "config": {"workload": "jacobi2d 8192x8192 T=160 (bounded CPU sample of config 4)",
                    "parallelism": "OpenMP tasks, %d threads" % threads},
         "cpu_baseline": {"value": value, "unit": "GUpdates/s", "cores": threads, "kind": kind,
-                         "sample": "Jacobi-2D 8192^2 T=32, reference emitted C"},
+                         "sample": "Jacobi-2D 8192^2 T=160, reference emitted C"},
         "e2e": {"value": value, "unit": "GUpdates/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }

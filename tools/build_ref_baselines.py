@@ -23,7 +23,7 @@ GCC = "/usr/bin/gcc" if os.path.exists("/usr/bin/gcc") else "gcc"
 
 # (tag, kernel, params, leaf sizes) — bounded samples of the BASELINE workloads
 SAMPLES = [
-    ("jacobi2d_N8192_T32", "jacobi2d", {"T": 32, "N": 8192}, (16, 128, 1024)),
+    ("jacobi2d_N8192_T160", "jacobi2d", {"T": 160, "N": 8192}, (16, 128, 1024)),
     ("jacobi2d_N8192_T0", "jacobi2d", {"T": 0, "N": 8192}, (1, 128, 1024)),
     ("heat3d_b_N384_T8", "heat3d_b", {"T": 8, "N": 384}, (8, 32, 32, 128)),
     ("heat3d_b_N384_T0", "heat3d_b", {"T": 0, "N": 384}, (1, 32, 32, 128)),
