@@ -215,6 +215,7 @@ def main():
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-depth-sweep", action="store_true")
     args = ap.parse_args()
     rank, world, local = env_rank()
 
@@ -287,6 +288,33 @@ def main():
             "avg_launch_ms": (sum(kms) / len(kms)) if kms else None,
             "launches_per_step": len(kms) // max(1, args.steps),
             "bytes_per_update": 16.0 / args.bt, "kernel_share_of_step": kernel_ms / ms if ms else None}
+
+    # the same kernel at shallower temporal depths (one warm + one timed step
+    # each, after the timed region): the throughput / HBM-fraction trade-off
+    depths = []
+    if world == 1 and not args.no_depth_sweep:
+        for bt in (4, 5):
+            if bt == args.bt:
+                continue
+            S.bt = bt
+            S.restart()
+            S.run()
+            S.kernel_events.clear()
+            torch.cuda.synchronize()
+            d0 = torch.cuda.Event(enable_timing=True)
+            d1 = torch.cuda.Event(enable_timing=True)
+            d0.record(stream)
+            S.restart()
+            S.run(record=True)
+            d1.record(stream)
+            torch.cuda.synchronize()
+            kms_bt = sum(x.elapsed_time(y) for x, y in S.kernel_events)
+            launches_bt = -(-args.T // bt)
+            depths.append({"bt": bt, "GUpd/s": round(updates / (d0.elapsed_time(d1) / 1e3) / 1e9, 1),
+                           "hbm_frac": round(16.0 * cells * launches_bt / (kms_bt / 1e3) / 1e9 / peak, 3)})
+        S.bt = args.bt
+        S.kernel_events.clear()
+    roof["depth_tradeoff"] = depths
 
     # e2e through the C ABI with host buffers (N=1: GpuExecutor; N>1: slab copies)
     e2e = None
