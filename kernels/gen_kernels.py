@@ -286,13 +286,134 @@ def gemm():
     return spec("gemm", ["N"], ["i", "j", "k"], {"N": 3}, arrays, sts)
 
 
+# ------------------------------------------------------- corpus restatements
+# The reference corpus kernels outside the hot-path registry, restated from
+# their documented semantics so the device interpreter (csrc/generic.cu) can
+# be tested without /root/reference (tests/golden/corpus.json pins each one to
+# the reference interpreter's checksum on the corpus file itself).
+
+def triangle():
+    """Prefix-style triangle recurrence: C[i, 0] = B[i]; C[i, j] = C[i-1, j-1]
+    + C[i, j-1] for 1 <= j <= i < N; Out[i] = C[i, i]."""
+    s = Space(["i", "j"], ["N"])
+    N1 = lin((1, "N"), const=-1)
+    i_all = s.between(lin((1, "i")), C(0), N1)
+    sts = [
+        stmt("S0", 2, i_all + s.eq(lin((1, "j")), C(0)), "C", ["i", "j"], "B[i]"),
+        stmt("S1", 2, [s.ge(lin((1, "j")), C(1)), s.ge(lin((1, "i")), lin((1, "j"))),
+                       s.ge(N1, lin((1, "i")))], "C", ["i", "j"], "C[i - 1, j - 1] + C[i, j - 1]"),
+        stmt("Sfin", 2, s.eq(lin((1, "i"), (-1, "j")), C(0)) + i_all, "Out", ["i"], "C[i, j]"),
+    ]
+    arrays = [
+        {"name": "B", "rank": 1, "extents": ["N"], "kind": "input"},
+        {"name": "C", "rank": 2, "extents": ["N", "N"], "kind": "temp"},
+        {"name": "Out", "rank": 1, "extents": ["N"], "kind": "output"},
+    ]
+    return spec("triangle", ["N"], ["i", "j"], {"N": 8}, arrays, sts)
+
+
+def heat1d_fig7():
+    """1-D heat with a coupling term to the left boundary cell (the paper's
+    figure-7 example): X[0, i] = F[i]; interior X[t, i] = 0.25*(X[t-1, i-1] +
+    X[t-1, i] + X[t-1, i+1] + X[t-1, 0]); both boundary cells copied forward
+    (the left one by a depth-1 statement over t only); Out = X[T, .]."""
+    s = Space(["t", "i"], ["T", "N"])
+    N1, N2 = lin((1, "N"), const=-1), lin((1, "N"), const=-2)
+    t_up = s.between(lin((1, "t")), C(1), lin((1, "T")))
+    s1 = Space(["t"], ["T", "N"])  # the depth-1 statement's own space
+    sts = [
+        stmt("S0", 2, s.eq(lin((1, "t")), C(0)) + s.between(lin((1, "i")), C(0), N1), "X",
+             ["t", "i"], "F[i]"),
+        stmt("S1", 2, t_up + s.between(lin((1, "i")), C(1), N2), "X", ["t", "i"],
+             "0.25 * (X[t - 1, i - 1] + X[t - 1, i] + X[t - 1, i + 1] + X[t - 1, 0])"),
+        stmt("S2", 1, s1.between(lin((1, "t")), C(1), lin((1, "T"))), "X", ["t", "0"],
+             "X[t - 1, 0]"),
+        stmt("S3", 2, t_up + s.eq(lin((1, "i")), N1), "X", ["t", "i"], "X[t - 1, i]"),
+        stmt("Sfin", 2, s.eq(lin((1, "t")), lin((1, "T"))) + s.between(lin((1, "i")), C(0), N1),
+             "Out", ["i"], "X[t, i]"),
+    ]
+    arrays = [
+        {"name": "F", "rank": 1, "extents": ["N"], "kind": "input"},
+        {"name": "X", "rank": 2, "extents": ["T + 1", "N"], "kind": "temp"},
+        {"name": "Out", "rank": 1, "extents": ["N"], "kind": "output"},
+    ]
+    k = spec("heat1d-fig7", ["T", "N"], ["t", "i"], {"T": 8, "N": 8}, arrays, sts)
+    k["tilable_band"] = [0]
+    return k
+
+
+def lud():
+    """LU decomposition without pivoting, single-assignment over k: level 0
+    copies M (diagonal + N), level k eliminates the trailing block, Out takes
+    U from level i (j >= i) and L from level j (i > j)."""
+    s = Space(["k", "i", "j"], ["N"])
+    N1 = lin((1, "N"), const=-1)
+    k0 = s.eq(lin((1, "k")), C(0))
+    upd = "A[k - 1, i, j] - A[k - 1, i, k - 1] * A[k - 1, k - 1, j] / A[k - 1, k - 1, k - 1]"
+    sts = [
+        stmt("S0d", 3, k0 + s.eq(lin((1, "i"), (-1, "j")), C(0)) + s.between(lin((1, "i")), C(0), N1),
+             "A", ["k", "i", "j"], "M[i, j] + N"),
+        stmt("S0l", 3, k0 + [s.ge(lin((1, "j"))), s.ge(lin((1, "i"), (-1, "j")), C(1)),
+                             s.ge(N1, lin((1, "i")))], "A", ["k", "i", "j"], "M[i, j]"),
+        stmt("S0u", 3, k0 + [s.ge(lin((1, "i"))), s.ge(lin((1, "j"), (-1, "i")), C(1)),
+                             s.ge(N1, lin((1, "j")))], "A", ["k", "i", "j"], "M[i, j]"),
+        stmt("S", 3, s.between(lin((1, "k")), C(1), N1) + s.between(lin((1, "i")), lin((1, "k")), N1)
+             + s.between(lin((1, "j")), lin((1, "k")), N1), "A", ["k", "i", "j"], upd),
+        stmt("SfU", 3, s.eq(lin((1, "k"), (-1, "i")), C(0)) + s.between(lin((1, "j")), lin((1, "i")), N1)
+             + [s.ge(lin((1, "i")))], "Out", ["i", "j"], "A[k, i, j]"),
+        stmt("SfL", 3, s.eq(lin((1, "k"), (-1, "j")), C(0)) + [s.ge(lin((1, "i"), (-1, "j")), C(1)),
+                                                              s.ge(N1, lin((1, "i"))), s.ge(lin((1, "j")))],
+             "Out", ["i", "j"], "A[k, i, j]"),
+    ]
+    arrays = [
+        {"name": "M", "rank": 2, "extents": ["N", "N"], "kind": "input"},
+        {"name": "A", "rank": 3, "extents": ["N", "N", "N"], "kind": "temp"},
+        {"name": "Out", "rank": 2, "extents": ["N", "N"], "kind": "output"},
+    ]
+    return spec("lud", ["N"], ["k", "i", "j"], {"N": 6}, arrays, sts)
+
+
+def osp():
+    """Optimal-split dynamic programme over interval length u and right end v:
+    C[v-1, v] = W[v-1]*W[v] (u = 1); for u >= 2 the running minimum Acc over
+    split points m, then C[v-u, v] = min + W[v-u]*W[v] (C is overwritten: the
+    interpreter runs it in the reference's order); Out[0] = C[0, N-1]."""
+    s = Space(["u", "v", "m"], ["N"])
+    s2 = Space(["u", "v"], ["N"])
+    N1 = lin((1, "N"), const=-1)
+    uv = s.between(lin((1, "u")), C(2), N1) + s.between(lin((1, "v")), lin((1, "u")), N1)
+    sts = [
+        stmt("Sb", 2, s2.eq(lin((1, "u")), C(1)) + s2.between(lin((1, "v")), C(1), N1), "C",
+             ["v - u", "v"], "W[v - u] * W[v]"),
+        stmt("Sa0", 3, uv + s.eq(lin((1, "m"), (-1, "v"), (1, "u")), C(1)), "Acc", ["u", "v", "m"],
+             "C[v - u, m] + C[m, v]"),
+        stmt("Sa", 3, uv + [s.ge(lin((1, "m"), (-1, "v"), (1, "u")), C(2)),
+                            s.ge(lin((1, "v"), (-1, "m")), C(1))], "Acc", ["u", "v", "m"],
+             "min(Acc[u, v, m - 1], C[v - u, m] + C[m, v])"),
+        stmt("Sc", 3, uv + s.eq(lin((1, "m"), (-1, "v")), C(-1)), "C", ["v - u", "v"],
+             "Acc[u, v, m] + W[v - u] * W[v]"),
+        stmt("Sfin", 3, s.eq(lin((1, "u")), N1) + s.eq(lin((1, "v")), N1)
+             + s.eq(lin((1, "m"), (-1, "v")), C(-1)), "Out", ["0"], "C[v - u, v]"),
+    ]
+    arrays = [
+        {"name": "W", "rank": 1, "extents": ["N"], "kind": "input"},
+        {"name": "C", "rank": 2, "extents": ["N", "N"], "kind": "temp"},
+        {"name": "Acc", "rank": 3, "extents": ["N", "N", "N"], "kind": "temp"},
+        {"name": "Out", "rank": 1, "extents": ["1"], "kind": "output"},
+    ]
+    k = spec("osp", ["N"], ["u", "v", "m"], {"N": 8}, arrays, sts)
+    k["tilable_band"] = [0, 1]
+    return k
+
+
 def dump(obj):
     """Compact rows, one statement field per line."""
     return json.dumps(obj, indent=1) + "\n"
 
 
 def main():
-    for fn in (jacobi2d, heat2d_hold, heat3d_hold, heat3d_b, gs2d, gemm):
+    for fn in (jacobi2d, heat2d_hold, heat3d_hold, heat3d_b, gs2d, gemm, triangle, heat1d_fig7,
+               lud, osp):
         k = fn()
         path = os.path.join(HERE, k["name"] + ".kernel")
         with open(path, "w") as f:

@@ -21,7 +21,7 @@ REPO = os.path.dirname(PKG)
 LIB_PATH = os.path.join(PKG, "libpcotgpu.so")
 KERNELS_DIR = os.path.join(REPO, "kernels")
 
-FAMILIES = {1: "stencil2d5", 2: "stencil3d7", 3: "gs2d9", 4: "gemm"}
+FAMILIES = {1: "stencil2d5", 2: "stencil3d7", 3: "gs2d9", 4: "gemm", 5: "generic"}
 SCHEMES = {"untiled": 0, "slt": 1, "cot": 2}
 # status -> reference pcot::ErrorKind name (error.hpp:8-16)
 ERROR_KINDS = {1: "Overflow", 2: "DimMismatch", 3: "Unbounded", 4: "Parse", 5: "Validation",

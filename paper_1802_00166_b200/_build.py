@@ -25,9 +25,10 @@ CU_FLAGS = {
     "gs2d.cu": ["-fmad=false"],
     "misc.cu": ["-fmad=false"],
     "dgemm.cu": [],
+    "generic.cu": ["-fmad=false"],
 }
 CPP = ["spec.cpp", "executor.cpp"]
-DEPS = ["common.cuh", "kernels.h", "spec.h"]
+DEPS = ["common.cuh", "kernels.h", "spec.h", "generic.h"]
 
 
 def _stale(out, srcs):

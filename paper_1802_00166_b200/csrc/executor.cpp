@@ -23,6 +23,7 @@
 #include <mutex>
 
 #include "../../include/pcotgpu.h"
+#include "generic.h"
 #include "kernels.h"
 
 namespace pcotgpu {
@@ -88,6 +89,15 @@ struct GpuExecutor::Impl {
   int64_t g_ld = 0;
   int result_slot = -1;  // which buffer holds the output after a run (-1: none)
   mutable std::map<std::string, std::vector<double>> mirror;
+  // generic device interpreter (kernels outside the hot-path registry)
+  bool generic = false;
+  GenericPlan* gplan = nullptr;
+  GenericCounts gcounts;
+  int garray(const std::string& a) const {
+    for (size_t i = 0; i < generic_array_count(gplan); ++i)
+      if (generic_array_name(gplan, i) == a) return int(i);
+    return -1;
+  }
   // batched host runs (run_batch): copy streams and device staging
   cudaStream_t h2d = nullptr, d2h = nullptr;
   cudaEvent_t e_start = nullptr, e_in = nullptr, e_prev = nullptr, e_out = nullptr, e_free = nullptr;
@@ -99,6 +109,7 @@ struct GpuExecutor::Impl {
     if (h2d) cudaStreamDestroy(h2d);
     if (d2h) cudaStreamDestroy(d2h);
     if (gs_plan) gs2d_plan_destroy(gs_plan);
+    if (gplan) generic_plan_destroy(gplan);
     if (ev0) cudaEventDestroy(ev0);
     if (ev1) cudaEventDestroy(ev1);
     if (own_stream && stream) cudaStreamDestroy(stream);
@@ -107,6 +118,7 @@ struct GpuExecutor::Impl {
   uint64_t words_of(const std::string& a) const {
     const ArrayDecl* d = spec.find_array(a);
     if (!d) fail(ErrorKind::Validation, "array_data: unknown array " + a);
+    if (generic) return generic_array_words(gplan, size_t(garray(a)));
     if (rec.family == Family::Gemm) return uint64_t(n) * uint64_t(n);
     uint64_t w = 1;
     for (int i = 0; i < rec.ndim; ++i) w *= uint64_t(n);
@@ -116,6 +128,16 @@ struct GpuExecutor::Impl {
 
   void init_inputs() {
     ck(cudaSetDevice(device), "cudaSetDevice");
+    if (generic) {
+      ck(generic_init_inputs(gplan, stream), "generic init");
+      for (size_t i = 0; i < generic_array_count(gplan); ++i)  // temps/outputs: 0.0
+        if (generic_array_kind(gplan, i) != ArrayKind::Input && generic_array_words(gplan, i))
+          ck(cudaMemsetAsync(generic_array_ptr(gplan, i), 0, generic_array_words(gplan, i) * 8, stream),
+             "cudaMemset");
+      ck(cudaStreamSynchronize(stream), "init inputs");
+      mirror.clear();
+      return;
+    }
     for (size_t q = 0; q < rec.inputs.size(); ++q) {
       const std::string& nm = rec.inputs[q];
       uint64_t h = fnv1a(nm.data(), nm.size());
@@ -142,6 +164,19 @@ struct GpuExecutor::Impl {
     ck(cudaEventCreate(&ev1), "cudaEventCreate");
     n = rec.N;
     T = rec.T;
+    if (generic) {
+      gplan = generic_plan_create(spec, params, device);
+      rec = Recognized();
+      rec.family = Family::Generic;
+      rec.ndim = 0;
+      for (const auto& a : spec.arrays) {
+        if (a.kind == ArrayKind::Input) rec.inputs.push_back(a.name);
+        if (a.kind == ArrayKind::Output && rec.output.empty()) rec.output = a.name;
+        if (a.kind == ArrayKind::Temp && rec.temp.empty()) rec.temp = a.name;
+      }
+      init_inputs();
+      return;
+    }
     switch (rec.family) {
       case Family::Stencil2D5: {
         in_ld = n;
@@ -288,6 +323,7 @@ struct GpuExecutor::Impl {
       case Family::Stencil3D7: r.bt = run_stencil3d(o); break;
       case Family::GaussSeidel2D9: r.bt = run_gs(o); break;
       case Family::Gemm: r.bt = run_gemm(o); break;
+      case Family::Generic: run_generic(); break;
     }
     ck(cudaEventRecord(ev1, stream), "cudaEventRecord");
     ck(cudaEventSynchronize(ev1), "run");
@@ -295,21 +331,48 @@ struct GpuExecutor::Impl {
     ck(cudaEventElapsedTime(&ms, ev0, ev1), "cudaEventElapsedTime");
     r.device_ms = ms;
     r.launches = launches() - l0;
-    r.points = rec.points;
-    r.reads = rec.reads;
-    r.writes = rec.writes;
+    r.points = generic ? gcounts.points : rec.points;
+    r.reads = generic ? gcounts.reads : rec.reads;
+    r.writes = generic ? gcounts.writes : rec.writes;
     mirror.clear();
     if (!opts.skip_checksum) {
-      const std::vector<double>& out = array_data(rec.output);
-      r.checksum = fnv1a(out.data(), out.size() * sizeof(double));
+      if (generic) {  // every Output array in declaration order (exec.cpp:492-495)
+        uint64_t h = 0xcbf29ce484222325ULL;
+        for (const auto& a : spec.arrays)
+          if (a.kind == ArrayKind::Output) {
+            const std::vector<double>& out = array_data(a.name);
+            h = fnv1a(out.data(), out.size() * sizeof(double), h);
+          }
+        r.checksum = h;
+      } else {
+        const std::vector<double>& out = array_data(rec.output);
+        r.checksum = fnv1a(out.data(), out.size() * sizeof(double));
+      }
     }
     return r;
   }
 
+  void run_generic() {
+    std::string msg;
+    cudaError_t e = generic_run(gplan, stream, &gcounts, &msg);
+    if (e == cudaErrorInvalidValue && !msg.empty()) fail(ErrorKind::Validation, msg);
+    ck(e, "generic run");
+    result_slot = 0;
+  }
+
   // ---------------------------------------------------------------- host <-> device
   // output device view: pointer + pitch (2-D), or copy-out for 3-D
+  void read_generic(int i, double* host) const {
+    const uint64_t w = generic_array_words(gplan, size_t(i));
+    if (w)
+      ck(cudaMemcpyAsync(host, generic_array_ptr(gplan, size_t(i)), w * 8, cudaMemcpyDeviceToHost, stream),
+         "D2H");
+    ck(cudaStreamSynchronize(stream), "D2H");
+  }
+
   void read_output(double* host) const {
     ck(cudaSetDevice(device), "cudaSetDevice");
+    if (generic) return read_generic(garray(rec.output), host);
     if (result_slot < 0) {  // never run: reference outputs start at 0.0
       std::memset(host, 0, words_of(rec.output) * sizeof(double));
       return;
@@ -409,6 +472,23 @@ struct GpuExecutor::Impl {
       for (size_t q = 0; q < ni; ++q)
         if (!hin || !hin[k * ni + q]) fail(ErrorKind::Validation, "run_batch: null input pointer");
     }
+    if (generic) {  // interpreter path: instances one after the other
+      ExecResult r;
+      double ms = 0;
+      uint64_t l0 = launches();
+      for (size_t k = 0; k < count; ++k) {
+        for (size_t q = 0; q < ni; ++q) write_input(int(q), hin[k * ni + q]);
+        ExecOptions o2 = opts;
+        o2.skip_checksum = true;
+        r = run(o, o2);
+        ms += r.device_ms;
+        read_output(hout[k]);
+      }
+      r.device_ms = ms;
+      r.launches = launches() - l0;
+      if (!opts.skip_checksum) r.checksum = fnv1a(hout[count - 1], words_of(rec.output) * sizeof(double));
+      return r;
+    }
     ck(cudaSetDevice(device), "cudaSetDevice");
     if (!h2d) {
       ck(cudaStreamCreateWithFlags(&h2d, cudaStreamNonBlocking), "cudaStreamCreate");
@@ -471,6 +551,7 @@ struct GpuExecutor::Impl {
 
   void read_input(int q, double* host) const {
     ck(cudaSetDevice(device), "cudaSetDevice");
+    if (generic) return read_generic(garray(rec.inputs[size_t(q)]), host);
     const uint64_t w = words_of(rec.inputs[q]);
     if (rec.ndim == 3)
       ck(cudaMemcpyAsync(host, in[q].p, w * 8, cudaMemcpyDeviceToHost, stream), "D2H");
@@ -482,6 +563,16 @@ struct GpuExecutor::Impl {
 
   void write_input(int q, const double* host) {
     ck(cudaSetDevice(device), "cudaSetDevice");
+    if (generic) {
+      const int i = garray(rec.inputs[size_t(q)]);
+      const uint64_t w = generic_array_words(gplan, size_t(i));
+      if (w)
+        ck(cudaMemcpyAsync(generic_array_ptr(gplan, size_t(i)), host, w * 8, cudaMemcpyHostToDevice, stream),
+           "H2D");
+      ck(cudaStreamSynchronize(stream), "H2D");
+      mirror.clear();
+      return;
+    }
     const uint64_t w = words_of(rec.inputs[q]);
     if (rec.ndim == 3)
       ck(cudaMemcpyAsync(in[q].p, host, w * 8, cudaMemcpyHostToDevice, stream), "H2D");
@@ -498,7 +589,8 @@ struct GpuExecutor::Impl {
     auto it = mirror.find(a);
     if (it != mirror.end()) return it->second;
     std::vector<double> v(words_of(a));
-    if (d->kind == ArrayKind::Output) read_output(v.data());
+    if (generic) read_generic(garray(a), v.data());  // dense storage: temps too
+    else if (d->kind == ArrayKind::Output) read_output(v.data());
     else if (d->kind == ArrayKind::Input) read_input(input_slot(a), v.data());
     else fail(ErrorKind::Unsupported, "array_data: temp array " + a + " lives in the device layout");
     return mirror.emplace(a, std::move(v)).first->second;
@@ -512,7 +604,17 @@ GpuExecutor::GpuExecutor(const KernelSpec& embedded, const IntVec& params,
   impl_->spec = embedded;
   impl_->params = params;
   impl_->device = device;
-  impl_->rec = recognize(embedded, params);
+  // Hot-path kernels go to their hand-written kernels; anything else the
+  // reference can run goes to the device interpreter (generic.h).
+  try {
+    impl_->rec = recognize(embedded, params);
+  } catch (const Error& e) {
+    const bool shallow = e.kind() == ErrorKind::Validation &&
+                         std::string(e.what()).find("embedded") != std::string::npos;
+    if (e.kind() != ErrorKind::Unsupported && !shallow) throw;
+    impl_->generic = true;
+  }
+  if (env_int("PCOTGPU_FORCE_GENERIC", 0)) impl_->generic = true;
   impl_->setup();
 }
 
@@ -565,12 +667,19 @@ double* GpuExecutor::device_view(const std::string& a, int64_t* ld) {
     if (ld) *ld = m.rec.ndim == 3 ? m.n : m.in_ld;
     return m.in[q].p;
   }
+  if (m.generic) {
+    const int i = m.garray(a);
+    if (i < 0) fail(ErrorKind::Validation, "device_view: unknown array " + a);
+    if (ld) *ld = int64_t(generic_array_words(m.gplan, size_t(i)));
+    return generic_array_ptr(m.gplan, size_t(i));
+  }
   if (a != m.rec.output || m.result_slot < 0) fail(ErrorKind::Validation, "device_view: no device data for " + a);
   switch (m.rec.family) {
     case Family::Stencil2D5: if (ld) *ld = m.sg[m.result_slot].ld; return m.sg[m.result_slot].origin;
     case Family::Stencil3D7: if (ld) *ld = m.cg[m.result_slot].pitch_j; return m.cg[m.result_slot].origin;
     case Family::GaussSeidel2D9: if (ld) *ld = m.gs_ld; return m.gsa.p;
     case Family::Gemm: if (ld) *ld = m.g_ld; return m.gC.p;
+    case Family::Generic: break;
   }
   return nullptr;
 }

@@ -1,0 +1,644 @@
+// Generic device executor: see generic.h.  Follows the reference's
+// Executor::exec_stmt / run_level semantics (core/src/exec.cpp:347-472): the
+// union of the statement domains is walked in lexicographic index order, each
+// point runs the statements that contain it in declaration order, and each
+// body is the postfix program of the reference's flatten (exec.cpp:187-224).
+#include <algorithm>
+#include <climits>
+#include <cmath>
+#include <cstring>
+#include <functional>
+#include <map>
+#include <memory>
+#include <numeric>
+
+#include "common.cuh"
+#include "generic.h"
+#include "kernels.h"
+
+namespace pcotgpu {
+
+namespace {
+
+constexpr int kMaxIdx = 6, kMaxRank = 6, kMaxStack = 32;
+constexpr long long kSpinCapG = 200000000LL;
+
+struct GAff {
+  int64_t c[kMaxIdx];
+  int64_t k;
+};
+struct GRef {
+  int array, rank, aff0, pad;
+  int64_t ext[kMaxRank], stride[kMaxRank];
+};
+enum GOpKind { OLit, OAff, ORead, OAdd, OSub, OMul, ODiv, OMin, OMax, ONeg, OSqrt };
+struct GOp {
+  int kind, arg;
+  double lit;
+};
+struct GStmt {
+  int row0, nrows, op0, nops, wref, nreads;
+};
+struct GDev {
+  int nidx, nstmt;
+  int64_t lo[kMaxIdx], ext[kMaxIdx], npoints;
+  const GStmt* st;
+  const GAff* rows;
+  const GAff* affs;
+  const GRef* refs;
+  const GOp* ops;
+  double* const* arr;
+  const int64_t* fbase;  // first flag of each array
+  unsigned* flags;       // dataflow: 1 = cell holds its final value; count pass: writes
+  unsigned long long* next;
+  unsigned long long* cnt;  // points, reads, writes
+  int* err;                 // 0 ok; s+1: out-of-extent in statement s; -1: wait cap
+};
+
+PCOT_DEV int64_t aff_eval(const GAff& a, const int64_t* z, int n) {
+  int64_t v = a.k;
+  for (int i = 0; i < n; ++i) v += a.c[i] * z[i];
+  return v;
+}
+
+PCOT_DEV bool in_domain(const GDev& g, const GStmt& s, const int64_t* z) {
+  for (int r = 0; r < s.nrows; ++r)
+    if (aff_eval(g.rows[s.row0 + r], z, g.nidx) < 0) return false;
+  return true;
+}
+
+PCOT_DEV bool cell_of(const GDev& g, const GRef& r, const int64_t* z, int64_t* flat) {
+  int64_t f = 0;
+  for (int d = 0; d < r.rank; ++d) {
+    const int64_t comp = aff_eval(g.affs[r.aff0 + d], z, g.nidx);
+    if (comp < 0 || comp >= r.ext[d]) return false;
+    f += comp * r.stride[d];
+  }
+  *flat = f;
+  return true;
+}
+
+PCOT_DEV void decode(const GDev& g, unsigned long long p, int64_t* z) {
+  for (int i = g.nidx - 1; i >= 0; --i) {
+    const unsigned long long e = (unsigned long long)g.ext[i];
+    z[i] = g.lo[i] + int64_t(p % e);
+    p /= e;
+  }
+}
+
+PCOT_DEV unsigned ld_acq_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+PCOT_DEV void st_rel_u32(unsigned* p, unsigned v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// Run every statement of point z.  Returns false on an error (recorded).
+template <bool DATAFLOW>
+PCOT_DEV bool exec_point(const GDev& g, const int64_t* z, unsigned long long* c3) {
+  for (int si = 0; si < g.nstmt; ++si) {
+    const GStmt s = g.st[si];
+    if (!in_domain(g, s, z)) continue;
+    double stk[kMaxStack];
+    int sp = 0;
+    for (int o = 0; o < s.nops; ++o) {
+      const GOp op = g.ops[s.op0 + o];
+      switch (op.kind) {
+        case OLit: stk[sp++] = op.lit; break;
+        case OAff: stk[sp++] = double(aff_eval(g.affs[op.arg], z, g.nidx)); break;
+        case ORead: {
+          const GRef& r = g.refs[op.arg];
+          int64_t f = 0;
+          if (!cell_of(g, r, z, &f)) {
+            atomicCAS(g.err, 0, si + 1);
+            return false;
+          }
+          if (DATAFLOW) {
+            const unsigned* fl = g.flags + g.fbase[r.array] + f;
+            long long it = 0;
+            while (ld_acq_u32(fl) == 0) {
+              if (++it > kSpinCapG) {
+                atomicCAS(g.err, 0, -1);
+                return false;
+              }
+              // a failed point never publishes its cell: stop waiting on error
+              if ((it & 255) == 0 && *reinterpret_cast<volatile int*>(g.err) != 0) return false;
+              __nanosleep(64);
+            }
+          }
+          stk[sp++] = __ldcg(g.arr[r.array] + f);
+          break;
+        }
+        case OAdd: --sp, stk[sp - 1] = __dadd_rn(stk[sp - 1], stk[sp]); break;
+        case OSub: --sp, stk[sp - 1] = __dsub_rn(stk[sp - 1], stk[sp]); break;
+        case OMul: --sp, stk[sp - 1] = __dmul_rn(stk[sp - 1], stk[sp]); break;
+        case ODiv: --sp, stk[sp - 1] = __ddiv_rn(stk[sp - 1], stk[sp]); break;
+        case OMin: {  // reference exec.cpp: b < a ? b : a
+          const double b = stk[--sp], a = stk[sp - 1];
+          stk[sp - 1] = b < a ? b : a;
+          break;
+        }
+        case OMax: {  // a < b ? b : a
+          const double b = stk[--sp], a = stk[sp - 1];
+          stk[sp - 1] = a < b ? b : a;
+          break;
+        }
+        case ONeg: stk[sp - 1] = -stk[sp - 1]; break;
+        case OSqrt: stk[sp - 1] = __dsqrt_rn(stk[sp - 1]); break;
+      }
+    }
+    const GRef& w = g.refs[s.wref];
+    int64_t f = 0;
+    if (!cell_of(g, w, z, &f)) {
+      atomicCAS(g.err, 0, si + 1);
+      return false;
+    }
+    __stcg(g.arr[w.array] + f, stk[sp - 1]);
+    if (DATAFLOW) st_rel_u32(g.flags + g.fbase[w.array] + f, 1u);
+    c3[0] += 1;
+    c3[1] += unsigned(s.nreads);
+    c3[2] += 1;
+  }
+  return true;
+}
+
+__global__ void generic_count_kernel(GDev g) {
+  int64_t z[kMaxIdx];
+  for (unsigned long long p = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x;
+       p < (unsigned long long)g.npoints; p += (unsigned long long)gridDim.x * blockDim.x) {
+    decode(g, p, z);
+    for (int si = 0; si < g.nstmt; ++si) {
+      const GStmt s = g.st[si];
+      if (!in_domain(g, s, z)) continue;
+      const GRef& w = g.refs[s.wref];
+      int64_t f = 0;
+      if (!cell_of(g, w, z, &f)) {
+        atomicCAS(g.err, 0, si + 1);
+        continue;
+      }
+      atomicAdd(g.flags + g.fbase[w.array] + f, 1u);
+    }
+  }
+}
+
+// flags <- (written at most... never written) ? ready : pending; max count
+__global__ void generic_flags_kernel(unsigned* flags, int64_t n, unsigned* maxc) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    const unsigned c = flags[i];
+    if (c > 1) atomicMax(maxc, c);
+    flags[i] = c == 0 ? 1u : 0u;
+  }
+}
+
+// Persistent dataflow grid: warps take 32 consecutive points in the
+// reference's order; reads wait for their cell's flag.
+__global__ void generic_dataflow_kernel(GDev g) {
+  const int lane = threadIdx.x & 31;
+  unsigned long long c3[3] = {0, 0, 0};
+  int64_t z[kMaxIdx];
+  bool ok = true;
+  for (;;) {
+    unsigned long long base = 0;
+    if (lane == 0) base = atomicAdd(g.next, 32ull);
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (base >= (unsigned long long)g.npoints) break;
+    const unsigned long long p = base + lane;
+    if (ok && p < (unsigned long long)g.npoints) {
+      decode(g, p, z);
+      ok = exec_point<true>(g, z, c3);
+    }
+  }
+  atomicAdd(&g.cnt[0], c3[0]);
+  atomicAdd(&g.cnt[1], c3[1]);
+  atomicAdd(&g.cnt[2], c3[2]);
+}
+
+// One thread, the reference's exact order (kernels that overwrite cells).
+__global__ void generic_sequential_kernel(GDev g) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  unsigned long long c3[3] = {0, 0, 0};
+  int64_t z[kMaxIdx];
+  for (unsigned long long p = 0; p < (unsigned long long)g.npoints; ++p) {
+    decode(g, p, z);
+    if (!exec_point<false>(g, z, c3)) break;
+  }
+  g.cnt[0] = c3[0];
+  g.cnt[1] = c3[1];
+  g.cnt[2] = c3[2];
+}
+
+// ---------------------------------------------------------------- host side
+int64_t floor_div(int64_t a, int64_t b) {  // b > 0
+  return a >= 0 ? a / b : -((-a + b - 1) / b);
+}
+int64_t ceil_div(int64_t a, int64_t b) { return -floor_div(-a, b); }
+
+using Row = std::vector<int64_t>;  // coefficients over n indices, then constant
+
+void normalize(Row& r) {
+  int64_t g = 0;
+  for (size_t i = 0; i + 1 < r.size(); ++i) g = std::gcd(g, r[i] < 0 ? -r[i] : r[i]);
+  if (g > 1) {
+    for (size_t i = 0; i + 1 < r.size(); ++i) r[i] /= g;
+    r.back() = floor_div(r.back(), g);  // integer tightening: a.z + k >= 0, a = g a'
+  }
+}
+
+// Bounds of index q over the integer points of {rows >= 0} (rational
+// Fourier-Motzkin relaxation, tightened).  Returns false if empty.
+bool project_bounds(std::vector<Row> rows, size_t n, size_t q, int64_t* lo, int64_t* hi,
+                    bool* bounded) {
+  for (size_t e = 0; e < n; ++e) {
+    if (e == q) continue;
+    std::vector<Row> pos, neg, keep;
+    for (auto& r : rows) (r[e] > 0 ? pos : r[e] < 0 ? neg : keep).push_back(r);
+    for (const auto& p : pos)
+      for (const auto& m : neg) {
+        Row c(n + 1);
+        const int64_t a = p[e], b = -m[e];
+        for (size_t i = 0; i <= n; ++i) c[i] = b * p[i] + a * m[i];
+        normalize(c);
+        keep.push_back(c);
+      }
+    std::sort(keep.begin(), keep.end());
+    keep.erase(std::unique(keep.begin(), keep.end()), keep.end());
+    if (keep.size() > 4000) fail(ErrorKind::Overflow, "GpuExecutor: domain projection too large");
+    rows.swap(keep);
+  }
+  int64_t L = INT64_MIN, H = INT64_MAX;
+  for (const auto& r : rows) {
+    if (r[q] > 0) L = std::max(L, ceil_div(-r.back(), r[q]));
+    else if (r[q] < 0) H = std::min(H, floor_div(r.back(), -r[q]));
+    else if (r.back() < 0) return false;
+  }
+  *bounded = L != INT64_MIN && H != INT64_MAX;
+  *lo = L;
+  *hi = H;
+  return L <= H;
+}
+
+}  // namespace
+
+struct GenericPlan {
+  int device = 0;
+  int nidx = 0;
+  std::vector<std::string> names;
+  std::vector<ArrayKind> kinds;
+  std::vector<uint64_t> words;
+  std::vector<double*> ptrs;
+  std::vector<int64_t> fbase;
+  int64_t nflags = 0;
+  std::vector<GStmt> st;
+  std::vector<GAff> rows, affs;
+  std::vector<GRef> refs;
+  std::vector<GOp> ops;
+  std::vector<std::string> stmt_ids;
+  int64_t lo[kMaxIdx] = {0}, ext[kMaxIdx] = {0};
+  int64_t npoints = 0;
+  // device copies
+  GStmt* d_st = nullptr;
+  GAff *d_rows = nullptr, *d_affs = nullptr;
+  GRef* d_refs = nullptr;
+  GOp* d_ops = nullptr;
+  double** d_arr = nullptr;
+  int64_t* d_fbase = nullptr;
+  unsigned* d_flags = nullptr;
+  unsigned* d_flags0 = nullptr;  // initial flags (dataflow)
+  unsigned long long* d_misc = nullptr;  // next, points, reads, writes
+  int* d_err = nullptr;
+  unsigned* d_maxc = nullptr;
+  bool dataflow = false;
+  bool counted = false;
+};
+
+namespace {
+
+void ckc(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) fail(ErrorKind::Cuda, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+template <class T>
+T* upload(const std::vector<T>& v) {
+  T* d = nullptr;
+  if (v.empty()) return nullptr;
+  ckc(cudaMalloc(&d, v.size() * sizeof(T)), "cudaMalloc");
+  ckc(cudaMemcpy(d, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice), "H2D");
+  return d;
+}
+
+// Affine over (depth indices ++ params) -> GAff over full indices with the
+// params folded into the constant (embedding: missing indices get 0).
+GAff fold(const Affine& a, size_t depth, size_t full, const IntVec& prm) {
+  GAff g;
+  std::memset(&g, 0, sizeof(g));
+  for (size_t i = 0; i < depth && i < a.c.size(); ++i) g.c[i] = a.c[i];
+  g.k = a.k;
+  for (size_t j = 0; j < prm.size(); ++j)
+    if (depth + j < a.c.size()) g.k += a.c[depth + j] * prm[j];
+  (void)full;
+  return g;
+}
+
+int64_t eval_extent(const Affine& a, size_t nidx, const IntVec& prm) {
+  int64_t v = a.k;
+  const size_t off = a.c.size() >= nidx + prm.size() ? nidx : 0;
+  for (size_t j = 0; j < prm.size(); ++j)
+    if (off + j < a.c.size()) v += a.c[off + j] * prm[j];
+  return v;
+}
+
+}  // namespace
+
+GenericPlan* generic_plan_create(const KernelSpec& k, const IntVec& prm, int device) {
+  if (prm.size() != k.params.size()) fail(ErrorKind::DimMismatch, "GpuExecutor: parameter count");
+  const size_t full = k.indices.size();
+  if (full == 0 || full > size_t(kMaxIdx)) fail(ErrorKind::Unsupported, "generic executor: 1..6 indices");
+  auto P = std::make_unique<GenericPlan>();
+  P->device = device;
+  P->nidx = int(full);
+  ckc(cudaSetDevice(device), "cudaSetDevice");
+  // ---- arrays (dense, declaration extents)
+  std::map<std::string, int> aid;
+  int64_t fb = 0;
+  for (const auto& a : k.arrays) {
+    if (a.rank > size_t(kMaxRank)) fail(ErrorKind::Unsupported, "generic executor: rank > 6");
+    uint64_t w = 1;
+    for (const auto& e : a.extents) {
+      const int64_t v = eval_extent(e, full, prm);
+      if (v < 0) fail(ErrorKind::Validation, "array " + a.name + ": negative extent");
+      w *= uint64_t(v);
+    }
+    if (w > (uint64_t(1) << 33)) fail(ErrorKind::Unsupported, "generic executor: array " + a.name + " too large for dense storage");
+    aid[a.name] = int(P->names.size());
+    P->names.push_back(a.name);
+    P->kinds.push_back(a.kind);
+    P->words.push_back(w);
+    P->fbase.push_back(fb);
+    fb += int64_t(w);
+    double* d = nullptr;
+    ckc(cudaMalloc(&d, std::max<uint64_t>(w, 1) * 8), "cudaMalloc");
+    P->ptrs.push_back(d);
+  }
+  P->nflags = fb;
+  auto make_ref = [&](const std::string& arr, const std::vector<Affine>& subs, size_t depth) {
+    const ArrayDecl* ad = k.find_array(arr);
+    GRef r;
+    std::memset(&r, 0, sizeof(r));
+    r.array = aid.at(arr);
+    r.rank = int(ad->rank);
+    r.aff0 = int(P->affs.size());
+    int64_t stride = 1;
+    for (int d = r.rank - 1; d >= 0; --d) {
+      r.ext[d] = eval_extent(ad->extents[size_t(d)], full, prm);
+      r.stride[d] = stride;
+      stride *= r.ext[d];
+    }
+    for (const auto& s : subs) P->affs.push_back(fold(s, depth, full, prm));
+    P->refs.push_back(r);
+    return int(P->refs.size() - 1);
+  };
+  // ---- statements: embed, fold params, compile bodies
+  std::vector<int64_t> lo(full, INT64_MAX), hi(full, INT64_MIN);
+  bool any = false;
+  for (const auto& s : k.statements) {
+    GStmt g;
+    std::memset(&g, 0, sizeof(g));
+    g.row0 = int(P->rows.size());
+    std::vector<Row> frows;
+    for (const auto& r : s.domain) {
+      Affine a;
+      a.c.assign(r.begin(), r.end() - 1);
+      a.k = r.back();
+      GAff ga = fold(a, s.depth, full, prm);
+      P->rows.push_back(ga);
+      Row fr(ga.c, ga.c + full);
+      fr.push_back(ga.k);
+      frows.push_back(fr);
+    }
+    for (size_t q = s.depth; q < full; ++q) {  // embed: z_q = 0
+      for (int sg : {1, -1}) {
+        GAff ga;
+        std::memset(&ga, 0, sizeof(ga));
+        ga.c[q] = sg;
+        P->rows.push_back(ga);
+        Row fr(full + 1, 0);
+        fr[q] = sg;
+        frows.push_back(fr);
+      }
+    }
+    g.nrows = int(P->rows.size()) - g.row0;
+    // point box: project the statement's domain on every index
+    bool empty = false;
+    std::vector<int64_t> slo(full), shi(full);
+    for (size_t q = 0; q < full && !empty; ++q) {
+      bool bounded = true;
+      if (!project_bounds(frows, full, q, &slo[q], &shi[q], &bounded)) empty = true;
+      else if (!bounded) fail(ErrorKind::Unbounded, "Executor: unbounded loop level in " + s.id);
+    }
+    if (!empty) {
+      any = true;
+      for (size_t q = 0; q < full; ++q) lo[q] = std::min(lo[q], slo[q]), hi[q] = std::max(hi[q], shi[q]);
+    }
+    // body -> postfix (left, right, op), reads counted statically
+    g.op0 = int(P->ops.size());
+    int nreads = 0;
+    std::function<void(const ExprPtr&)> emit = [&](const ExprPtr& e) {
+      GOp op;
+      op.arg = 0;
+      op.lit = 0.0;
+      switch (e->kind) {
+        case Expr::Kind::Lit: op.kind = OLit; op.lit = e->lit; break;
+        case Expr::Kind::Aff:
+          op.kind = OAff;
+          op.arg = int(P->affs.size());
+          P->affs.push_back(fold(e->aff, s.depth, full, prm));
+          break;
+        case Expr::Kind::Read:
+          op.kind = ORead;
+          op.arg = make_ref(e->array, e->subs, s.depth);
+          ++nreads;
+          break;
+        case Expr::Kind::Neg: emit(e->l); op.kind = ONeg; break;
+        case Expr::Kind::Sqrt: emit(e->l); op.kind = OSqrt; break;
+        default:
+          emit(e->l);
+          emit(e->r);
+          op.kind = e->kind == Expr::Kind::Add ? OAdd : e->kind == Expr::Kind::Sub ? OSub
+                  : e->kind == Expr::Kind::Mul ? OMul : e->kind == Expr::Kind::Div ? ODiv
+                  : e->kind == Expr::Kind::Min ? OMin : OMax;
+          break;
+      }
+      P->ops.push_back(op);
+    };
+    emit(s.body);
+    g.nops = int(P->ops.size()) - g.op0;
+    g.nreads = nreads;
+    // stack depth bound (postfix: pushes minus pops)
+    int sp = 0, mx = 0;
+    for (int o = g.op0; o < g.op0 + g.nops; ++o) {
+      const int kd = P->ops[size_t(o)].kind;
+      sp += (kd == OLit || kd == OAff || kd == ORead) ? 1 : (kd == ONeg || kd == OSqrt) ? 0 : -1;
+      mx = std::max(mx, sp);
+    }
+    if (mx > kMaxStack) fail(ErrorKind::Unsupported, "generic executor: expression too deep in " + s.id);
+    g.wref = make_ref(s.write_array, s.write_subs, s.depth);
+    P->st.push_back(g);
+    P->stmt_ids.push_back(s.id);
+  }
+  P->npoints = 0;
+  if (any) {
+    P->npoints = 1;
+    for (size_t q = 0; q < full; ++q) {
+      P->lo[q] = lo[q];
+      P->ext[q] = hi[q] - lo[q] + 1;
+      if (P->ext[q] <= 0 || P->npoints > (int64_t(1) << 50) / P->ext[q])
+        fail(ErrorKind::Overflow, "generic executor: iteration box too large");
+      P->npoints *= P->ext[q];
+    }
+  }
+  P->d_st = upload(P->st);
+  P->d_rows = upload(P->rows);
+  P->d_affs = upload(P->affs);
+  P->d_refs = upload(P->refs);
+  P->d_ops = upload(P->ops);
+  P->d_arr = upload(P->ptrs);
+  P->d_fbase = upload(P->fbase);
+  ckc(cudaMalloc(&P->d_flags, std::max<int64_t>(P->nflags, 1) * sizeof(unsigned)), "cudaMalloc");
+  ckc(cudaMalloc(&P->d_flags0, std::max<int64_t>(P->nflags, 1) * sizeof(unsigned)), "cudaMalloc");
+  ckc(cudaMalloc(&P->d_misc, 4 * sizeof(unsigned long long)), "cudaMalloc");
+  ckc(cudaMalloc(&P->d_err, sizeof(int)), "cudaMalloc");
+  ckc(cudaMalloc(&P->d_maxc, sizeof(unsigned)), "cudaMalloc");
+  return P.release();
+}
+
+void generic_plan_destroy(GenericPlan* p) {
+  if (!p) return;
+  for (double* d : p->ptrs) cudaFree(d);
+  cudaFree(p->d_st);
+  cudaFree(p->d_rows);
+  cudaFree(p->d_affs);
+  cudaFree(p->d_refs);
+  cudaFree(p->d_ops);
+  cudaFree(p->d_arr);
+  cudaFree(p->d_fbase);
+  cudaFree(p->d_flags);
+  cudaFree(p->d_flags0);
+  cudaFree(p->d_misc);
+  cudaFree(p->d_err);
+  cudaFree(p->d_maxc);
+  delete p;
+}
+
+size_t generic_array_count(const GenericPlan* p) { return p->names.size(); }
+const std::string& generic_array_name(const GenericPlan* p, size_t i) { return p->names[i]; }
+ArrayKind generic_array_kind(const GenericPlan* p, size_t i) { return p->kinds[i]; }
+uint64_t generic_array_words(const GenericPlan* p, size_t i) { return p->words[i]; }
+double* generic_array_ptr(GenericPlan* p, size_t i) { return p->ptrs[i]; }
+
+cudaError_t generic_init_inputs(GenericPlan* p, cudaStream_t s) {
+  cudaError_t e;
+  for (size_t i = 0; i < p->names.size(); ++i) {
+    if (p->kinds[i] != ArrayKind::Input || p->words[i] == 0) continue;
+    const uint64_t h = fnv1a(p->names[i].data(), p->names[i].size());
+    if ((e = fill_init_value(p->ptrs[i], int64_t(p->words[i]), 1, int64_t(p->words[i]), h, 0, s)) !=
+        cudaSuccess)
+      return e;
+  }
+  return cudaSuccess;
+}
+
+static GDev dev_args(GenericPlan* p) {
+  GDev g;
+  std::memset(&g, 0, sizeof(g));
+  g.nidx = p->nidx;
+  g.nstmt = int(p->st.size());
+  for (int i = 0; i < p->nidx; ++i) g.lo[i] = p->lo[i], g.ext[i] = p->ext[i];
+  g.npoints = p->npoints;
+  g.st = p->d_st;
+  g.rows = p->d_rows;
+  g.affs = p->d_affs;
+  g.refs = p->d_refs;
+  g.ops = p->d_ops;
+  g.arr = p->d_arr;
+  g.fbase = p->d_fbase;
+  g.flags = p->d_flags;
+  g.next = p->d_misc;
+  g.cnt = p->d_misc + 1;
+  g.err = p->d_err;
+  return g;
+}
+
+cudaError_t generic_run(GenericPlan* p, cudaStream_t s, GenericCounts* counts, std::string* err_msg) {
+  cudaError_t e;
+  GDev g = dev_args(p);
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, p->device);
+  // temps and outputs start at 0.0 every run (inputs persist)
+  for (size_t i = 0; i < p->names.size(); ++i)
+    if (p->kinds[i] != ArrayKind::Input && p->words[i])
+      if ((e = cudaMemsetAsync(p->ptrs[i], 0, p->words[i] * 8, s)) != cudaSuccess) return e;
+  if ((e = cudaMemsetAsync(p->d_err, 0, sizeof(int), s)) != cudaSuccess) return e;
+  if ((e = cudaMemsetAsync(p->d_misc, 0, 4 * sizeof(unsigned long long), s)) != cudaSuccess) return e;
+  if (!p->counted) {  // write counts once per plan: single assignment -> dataflow grid
+    if ((e = cudaMemsetAsync(p->d_flags, 0, std::max<int64_t>(p->nflags, 1) * sizeof(unsigned), s)) != cudaSuccess)
+      return e;
+    if ((e = cudaMemsetAsync(p->d_maxc, 0, sizeof(unsigned), s)) != cudaSuccess) return e;
+    if (p->npoints > 0) {
+      generic_count_kernel<<<sms * 8, 256, 0, s>>>(g);
+      count_launch();
+    }
+    if (p->nflags > 0) {
+      generic_flags_kernel<<<sms * 4, 256, 0, s>>>(p->d_flags, p->nflags, p->d_maxc);
+      count_launch();
+    }
+    unsigned maxc = 0;
+    int err = 0;
+    if ((e = cudaMemcpyAsync(&maxc, p->d_maxc, sizeof(unsigned), cudaMemcpyDeviceToHost, s)) != cudaSuccess) return e;
+    if ((e = cudaMemcpyAsync(&err, p->d_err, sizeof(int), cudaMemcpyDeviceToHost, s)) != cudaSuccess) return e;
+    if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return e;
+    if (err > 0) {
+      if (err_msg) *err_msg = "out-of-extent write in statement " + p->stmt_ids[size_t(err - 1)];
+      return cudaErrorInvalidValue;
+    }
+    p->dataflow = maxc <= 1;
+    if ((e = cudaMemcpyAsync(p->d_flags0, p->d_flags, std::max<int64_t>(p->nflags, 1) * sizeof(unsigned),
+                             cudaMemcpyDeviceToDevice, s)) != cudaSuccess)
+      return e;
+    p->counted = true;
+  } else if (p->dataflow) {
+    if ((e = cudaMemcpyAsync(p->d_flags, p->d_flags0, std::max<int64_t>(p->nflags, 1) * sizeof(unsigned),
+                             cudaMemcpyDeviceToDevice, s)) != cudaSuccess)
+      return e;
+  }
+  if (p->npoints > 0) {
+    if (p->dataflow) {
+      generic_dataflow_kernel<<<sms * 4, 128, 0, s>>>(g);
+    } else {
+      generic_sequential_kernel<<<1, 32, 0, s>>>(g);
+    }
+    count_launch();
+  }
+  unsigned long long c[3] = {0, 0, 0};
+  int err = 0;
+  if ((e = cudaMemcpyAsync(c, p->d_misc + 1, sizeof(c), cudaMemcpyDeviceToHost, s)) != cudaSuccess) return e;
+  if ((e = cudaMemcpyAsync(&err, p->d_err, sizeof(int), cudaMemcpyDeviceToHost, s)) != cudaSuccess) return e;
+  if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return e;
+  if (err != 0) {
+    if (err_msg)
+      *err_msg = err > 0 ? "out-of-extent access in statement " + p->stmt_ids[size_t(err - 1)]
+                         : std::string("dataflow wait exceeded its bound (kernel not legal in lexicographic order)");
+    return cudaErrorInvalidValue;
+  }
+  if (counts) {
+    counts->points = c[0];
+    counts->reads = c[1];
+    counts->writes = c[2];
+    counts->parallel = p->dataflow;
+  }
+  return cudaSuccess;
+}
+
+}  // namespace pcotgpu

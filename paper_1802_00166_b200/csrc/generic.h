@@ -1,0 +1,60 @@
+// Generic device execution of any embedded-or-embeddable PRDG kernel (the
+// reference's Executor semantics, core/src/exec.cpp:347-498) for kernels the
+// hot-path recognizer does not map onto a hand-written kernel (SURVEY §8f.2:
+// the remaining corpus kernels — triangle, lud, osp, heat1d-fig7 — run on the
+// device instead of being rejected).
+//
+// Storage: every array dense at its declared extents (the reference's
+// single-assignment layout, exec.cpp:234-245 without memory maps).
+// Schedule:
+//   * single-assignment kernels (every cell written at most once — checked on
+//     the device by a write-count pass): a persistent grid takes points in the
+//     reference's lexicographic order from an atomic counter; every read waits
+//     for its cell's ready flag (acquire), every write publishes it (release).
+//     A read only ever waits on a point earlier in that order, which is
+//     already running or done, so the grid cannot deadlock;
+//   * otherwise (cells overwritten, e.g. osp's C): one device thread walks the
+//     points in the reference's order.
+// Per point, the statements whose domains contain it run in declaration
+// order; bodies are evaluated as the reference's postfix program (one IEEE
+// rounding per operation, no contraction), so outputs are bit-identical.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "spec.h"
+
+namespace pcotgpu {
+
+struct GenericPlan;
+
+// Parse-time plan at a parameter binding: embeds shallow statements
+// (reference prdg.cpp:72-119: missing inner indices pinned to 0), evaluates
+// extents, projects every statement domain onto each index (Fourier-Motzkin)
+// for the point box, compiles bodies to postfix programs.  Throws Unbounded /
+// Validation like the reference.
+GenericPlan* generic_plan_create(const KernelSpec& k, const IntVec& params, int device);
+void generic_plan_destroy(GenericPlan* p);
+
+// Array access (dense, declaration extents).
+size_t generic_array_count(const GenericPlan* p);
+const std::string& generic_array_name(const GenericPlan* p, size_t i);
+ArrayKind generic_array_kind(const GenericPlan* p, size_t i);
+uint64_t generic_array_words(const GenericPlan* p, size_t i);
+double* generic_array_ptr(GenericPlan* p, size_t i);
+
+// Inputs <- init_value, temps/outputs <- 0.0 (reference init_storage,
+// exec.cpp:281-294); the inputs are kept, everything else is reset per run.
+cudaError_t generic_init_inputs(GenericPlan* p, cudaStream_t s);
+struct GenericCounts {
+  uint64_t points = 0, reads = 0, writes = 0;
+  bool parallel = false;  // dataflow grid (true) or sequential walk
+};
+// One run.  Errors: cudaErrorInvalidValue with `err_msg` set for an
+// out-of-extent access (reference exec.cpp:318-323).
+cudaError_t generic_run(GenericPlan* p, cudaStream_t s, GenericCounts* counts, std::string* err_msg);
+
+}  // namespace pcotgpu

@@ -58,6 +58,7 @@ const char* family_name(Family f) {
     case Family::Stencil3D7: return "stencil3d7";
     case Family::GaussSeidel2D9: return "gs2d9";
     case Family::Gemm: return "gemm";
+    case Family::Generic: return "generic";
   }
   return "?";
 }

@@ -88,7 +88,9 @@ std::string find_kernel_file(const std::string& name_or_path);
 ExprPtr parse_expr(const std::string& text, const std::vector<std::string>& indices,
                    const std::vector<std::string>& params);
 
-enum class Family { Stencil2D5 = 1, Stencil3D7 = 2, GaussSeidel2D9 = 3, Gemm = 4 };
+// Generic: any other embeddable kernel, run by the device interpreter
+// (generic.h) instead of a hand-written hot-path kernel.
+enum class Family { Stencil2D5 = 1, Stencil3D7 = 2, GaussSeidel2D9 = 3, Gemm = 4, Generic = 5 };
 
 struct StmtBox {
   std::string id;
