@@ -81,9 +81,10 @@ def test_s3d7_variants_bit_exact(variant):
         "    want = O.reference_output(k, {'T': 9, 'N': 77})\n"
         "    with P.GpuExecutor(O.kernel_path(k), {'T': 9, 'N': 77}) as ex:\n"
         "        for bt in range(1, 5):\n"
-        "            ex.run('slt', [bt, 8, 8, 8], skip_checksum=True)\n"
-        "            out = ex.array_data('Out')\n"
-        "            assert np.array_equal(out.view(np.uint64), want.view(np.uint64)), (k, bt)\n"
+        "            for sch in ('slt', 'cot'):\n"
+        "                ex.run(sch, [bt, 8, 8, 8], skip_checksum=True)\n"
+        "                out = ex.array_data('Out')\n"
+        "                assert np.array_equal(out.view(np.uint64), want.view(np.uint64)), (k, bt, sch)\n"
         "print('ok')\n")
     env = dict(**__import__("os").environ, PCOTGPU_S3D7_VARIANT=str(variant))
     p = subprocess.run([sys.executable, "-c", code], cwd=O.REPO, env=env, capture_output=True,
