@@ -35,7 +35,7 @@ EMIT_DIR = os.path.join(REPO, "oracle", "_ref", "emit")
 SAMPLE = "jacobi2d_N8192_T160"
 SAMPLE_INIT = "jacobi2d_N8192_T0"
 SAMPLE_UPDATES = 8192 * 8192 * 160
-METRIC = "stencil GUpdates/s"
+METRIC = "stencil GUpdates/s at 1/2/4/8 B200; % HBM roofline; DRAM bytes/update"  # BASELINE.json
 
 
 def env_rank():
@@ -287,7 +287,8 @@ def main():
             "kernel": "s2d5_kernel<bt=%d>" % args.bt, "peak_source": peak_src,
             "avg_launch_ms": (sum(kms) / len(kms)) if kms else None,
             "launches_per_step": len(kms) // max(1, args.steps),
-            "bytes_per_update": 16.0 / args.bt, "kernel_share_of_step": kernel_ms / ms if ms else None}
+            "bytes_per_update": 16.0 / args.bt, "kernel_share_of_step": kernel_ms / ms if ms else None,
+            "dram_bytes_per_update": (traffic["bytes_per_launch"] / (cells * args.bt)) if traffic else None}
 
     # the same kernel at shallower temporal depths (one warm + one timed step
     # each, after the timed region): the throughput / HBM-fraction trade-off
