@@ -49,7 +49,15 @@ def _ncu_cell(kernel, params, scheme, tile):
            "x".join(map(str, tile)), "--schemes", scheme, "--samples", "1", "--quiet",
            "--no-warmup"]
     p = subprocess.run(cmd, capture_output=True, text=True, cwd=REPO)
-    rows = [r for r in csv.reader(io.StringIO(p.stdout)) if len(r) > 10]
+    return parse_ncu_csv(p.stdout)
+
+
+def parse_ncu_csv(text):
+    """(DRAM bytes, sector-weighted L2 hit %) summed over the launches of an
+    `ncu --metrics ... --csv` listing (also used on captures made one cell per
+    process: `ncu ... python -m paper_1802_00166_b200.sweep ... --samples 1
+    --quiet --no-warmup > cell.csv`)."""
+    rows = [r for r in csv.reader(io.StringIO(text)) if len(r) > 10]
     if not rows:
         return None, None
     h = rows[0]
