@@ -304,7 +304,9 @@ struct GpuExecutor::Impl {
   }
 
   int run_gemm(const TileOrder& o) {
-    const int order = o.scheme == Scheme::Cot ? kOrderMorton : kOrderLex;
+    // untiled default: the recursive (Morton) CTA order — same time, up to 44%
+    // less DRAM traffic once A and B exceed the L2 (profiles/sweep_slt_cot_r01.md)
+    const int order = o.scheme == Scheme::Slt ? kOrderLex : kOrderMorton;
     ck(affine_2x_minus_1(in[0].p, gA.p, n * g_ld, stream), "affine A");
     ck(affine_2x_minus_1(in[1].p, gB.p, n * g_ld, stream), "affine B");
     ck(dgemm_nn(gA.p, gB.p, gC.p, n, g_ld, order, stream), "dgemm");
