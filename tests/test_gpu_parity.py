@@ -87,6 +87,19 @@ def test_gs2d_pipeline_matches_oracle(monkeypatch, variant, T, N):
     assert np.array_equal(got.view(np.uint64), want.view(np.uint64))
 
 
+def test_gs2d_pipeline_multi_launch_segments():
+    """T beyond one launch's level budget (progress words / band count): the
+    pipeline splits the sweeps into launches that restart from the grid."""
+    N, T = 130, 5000
+    F = O.init_array("F", N * N)
+    want = O.gs2d9(N, T, F)
+    with P.GpuExecutor("gs2d", {"T": T, "N": N}) as ex:
+        r = ex.run_untiled()
+        assert r.bt == 0 and r.launches >= 2 + 3  # copy-in + ring, then >= 3 segment launches
+        got = ex.array_data("Out")
+    assert np.array_equal(got.view(np.uint64), want.view(np.uint64))
+
+
 @pytest.mark.parametrize("variant", [0, 1, 2])
 @pytest.mark.parametrize("T,N", [(16, 1024), (64, 4096)])
 def test_gs2d_pipeline_goldens_repeated(monkeypatch, variant, T, N):
