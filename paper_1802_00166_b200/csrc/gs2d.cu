@@ -452,20 +452,9 @@ struct PipeArgs {
   int64_t ebld;     // edge-row stride (even, >= n + 2)
   int n, T, nb;
   int nclk;         // clocks per level (c = -1 .. n + 61)
-  long long* prof;  // optional per-warp cycle counters [nb * NW][8] (PCOTGPU_GS_PROF)
+  long long* prof;  // optional per-warp counters [nb * NW][16] (PCOTGPU_GS_PROF dev aid)
   int spin_ns;      // edge-poll backoff cap (ns)
 };
-
-// 16-byte async copy that bypasses L1 (.cg): the sources are written by other
-// warps/CTAs during the kernel, so no stale L1 line may serve them.
-PCOT_DEV void cp16(void* dst, const void* src) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src));
-}
-
-PCOT_DEV void cp_commit() { asm volatile("cp.async.commit_group;"); }
-PCOT_DEV void cp_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
-PCOT_DEV void cp_wait2() { asm volatile("cp.async.wait_group 2;" ::: "memory"); }
-PCOT_DEV void cp_wait0() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 
 // CTA-scope acquire/release on the shared-memory progress words: the acquire
 // load is a plain LDS (no fence), the release a CTA membar + STS.
@@ -955,7 +944,7 @@ cudaError_t gs2d_pipe_launch(GsPlan* p, const PipeVariant& v, size_t smem, doubl
     cudaStreamSynchronize(stream);
     cudaFree(g.prof);
     static const char* names[8] = {"wait_xcta", "wait_wrap", "wait_prod", "wait_ring",
-                                   "cp_wait",   "compute",   "publish",  "stage_in"};
+                                   "sync",      "compute",   "publish",  "stage_in"};
     double tot[8] = {0}, all = 0;
     for (size_t q = 0; q < np / 16; ++q)
       for (int m = 0; m < 8; ++m) tot[m] += double(h[q * 16 + m]), all += double(h[q * 16 + m]);
