@@ -542,6 +542,7 @@ __global__ void __launch_bounds__(NW * 32, 1) gs2d_pipe_kernel(PipeArgs g) {
   const int cmask = lane == 0 ? SG - 1 : dmask;
   long long pacc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   long long t_first = 0, c_first = 0;  // globaltimer / clock64 at the first compute (prof)
+  const long long t_entry = g.prof ? globaltimer() : 0;
   for (int t = w + 1; t <= g.T; t += NW) {
     const int i = i0 - (t - 1) + lane;  // this lane's row at level t
     const bool row_ok = i >= 1 && i <= g.n - 2;
@@ -724,6 +725,10 @@ __global__ void __launch_bounds__(NW * 32, 1) gs2d_pipe_kernel(PipeArgs g) {
     g.prof[(int64_t(b) * NW + w) * 16 + 9] = globaltimer();
     g.prof[(int64_t(b) * NW + w) * 16 + 10] = c_first;
     g.prof[(int64_t(b) * NW + w) * 16 + 11] = clock64();
+    g.prof[(int64_t(b) * NW + w) * 16 + 12] = t_entry;
+    unsigned smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    g.prof[(int64_t(b) * NW + w) * 16 + 13] = smid;
   }
 }
 
@@ -971,6 +976,15 @@ cudaError_t gs2d_pipe_launch(GsPlan* p, const PipeVariant& v, size_t smem, doubl
         fprintf(stderr, " b%d[%.1f,%.1f]", b, (h[(size_t(b) * v.nw) * 16 + 8] - t0) * 1e-3,
                 (h[(size_t(b) * v.nw + v.nw - 1) * 16 + 9] - t0) * 1e-3);
       }
+      long long emin = h[12], emax = h[12];
+      int late = 0;
+      for (int bb = 0; bb < nb; ++bb) {
+        const long long e = h[(size_t(bb) * v.nw) * 16 + 12];
+        emin = std::min(emin, e), emax = std::max(emax, e);
+      }
+      for (int bb = 0; bb < nb; ++bb)
+        if (h[(size_t(bb) * v.nw) * 16 + 12] - emin > 20000) ++late;
+      fprintf(stderr, "\n  CTA entry spread %.1f us (%d CTAs > 20 us late)", (emax - emin) * 1e-3, late);
       fprintf(stderr, "\n  band 0 warp 0 clock: %.0f MHz\n",
               double(h[11] - h[10]) / double(h[9] - h[8]) * 1e3);
     }
