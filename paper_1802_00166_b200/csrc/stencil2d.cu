@@ -352,7 +352,7 @@ cudaError_t launch_bt(const S2Args& a, int ring_hold, int rows, int variant, cud
     if (int64_t(rows) * a.cols <= (int64_t(1) << 24))
       variant = 9;  // small grids: narrow strips so the launch fills 148 SMs
     else
-      variant = BT <= 5 ? 6 : BT == 6 ? 5 : 4;
+      variant = BT <= 5 ? 6 : BT == 6 ? 11 : 4;
   }
   switch (variant) {
     case 1: return launch_cfg<BT, 2, 256, 2, false>(a, ring_hold, rows, s);
@@ -365,6 +365,8 @@ cudaError_t launch_bt(const S2Args& a, int ring_hold, int rows, int variant, cud
     case 8: return launch_cfg<BT, 2, 128, 4, true>(a, ring_hold, rows, s);
     case 9: return launch_cfg<BT, 2, 64, 8, true>(a, ring_hold, rows, s);
     case 10: return launch_cfg<BT, 4, 64, 6, true>(a, ring_hold, rows, s);
+    case 11: return launch_cfg<BT, 4, 96, 4, true>(a, ring_hold, rows, s);
+
     default: return launch_cfg<BT, 4, 128, 2, false>(a, ring_hold, rows, s);
   }
 }

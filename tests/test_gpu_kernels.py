@@ -92,7 +92,7 @@ def test_s3d7_variants_bit_exact(variant):
     assert p.returncode == 0 and "ok" in p.stdout, p.stdout + p.stderr
 
 
-@pytest.mark.parametrize("variant", [0, 1, 2, 3, 4, 5, 6, 7, 8])
+@pytest.mark.parametrize("variant", [0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11])
 def test_s2d5_variants_bit_exact(variant, monkeypatch):
     """Every compiled (C, NT, MINB) variant of the 2-D kernel, all depths."""
     import subprocess
