@@ -484,6 +484,19 @@ PCOT_DEV void wait_smem(const volatile int* p, int target) {
     __nanosleep(8);
 }
 
+// Same wait through a per-warp cache of the last value seen: progress words
+// only grow, and an earlier acquire of a value >= target already orders the
+// reads that need it, so a producer running ahead costs no shared load.
+PCOT_DEV void wait_seen(const volatile int* p, int target, int& seen) {
+  if (seen >= target) return;
+  int v = vld(p);
+  for (long long it = 0; !__all_sync(0xffffffffu, v >= target) && it < kSpinCap; ++it) {
+    __nanosleep(8);
+    v = vld(p);
+  }
+  seen = v;
+}
+
 // Cross-CTA edge values are polled as data: every slot of the edge arrays
 // starts as kEmpty (bytes 0xff, a NaN bit pattern the arithmetic never
 // produces — the device returns the canonical NaN 0x7fff...) and is written
@@ -541,6 +554,7 @@ __global__ void __launch_bounds__(NW * 32, 1) gs2d_pipe_kernel(PipeArgs g) {
   const int dmask = w ? RS - 1 : IRS - 1;
   const int cmask = lane == 0 ? SG - 1 : dmask;
   long long pacc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  int seen_prod = 0, seen_cons = 0, seen_wrap = 0;  // progress words last observed
   long long t_first = 0, c_first = 0;  // globaltimer / clock64 at the first compute (prof)
   const long long t_entry = g.prof ? globaltimer() : 0;
   for (int t = w + 1; t <= g.T; t += NW) {
@@ -631,7 +645,7 @@ __global__ void __launch_bounds__(NW * 32, 1) gs2d_pipe_kernel(PipeArgs g) {
 #pragma unroll
         for (int m = 1; m <= S / 2; ++m) store_pair(k, m, pre[m - 1]);
         if (k + 1 < nchunk) {
-          if (t > 1) wait_smem(prog + NW - 1, plvl + need(c_hi + S + 2));
+          if (t > 1) wait_seen(prog + NW - 1, plvl + need(c_hi + S + 2), seen_wrap);
           PCOT_PROF(1);
 #pragma unroll
           for (int m = 1; m <= S / 2; ++m) pre[m - 1] = load_pair(k + 1, m);
@@ -640,7 +654,7 @@ __global__ void __launch_bounds__(NW * 32, 1) gs2d_pipe_kernel(PipeArgs g) {
       PCOT_PROF(7);
       // producer ahead: D of clock c is producer lane l's column j+1, computed
       // at the producer's clock c+1
-      if (w > 0) wait_smem(prog + w - 1, plvl + need(c_hi + 2));
+      if (w > 0) wait_seen(prog + w - 1, plvl + need(c_hi + 2), seen_prod);
       PCOT_PROF(2);
       if (w < NW - 1) {
         // ring reuse: the consumer (level t+1) must have read what this chunk
@@ -649,9 +663,9 @@ __global__ void __launch_bounds__(NW * 32, 1) gs2d_pipe_kernel(PipeArgs g) {
         // t+1, since every slot is written, out-of-range columns included.
         const int rel = c_hi + 1 - (RS - 4);
         if (rel > 0) {
-          if (t + 1 <= g.T) wait_smem(prog + w + 1, clvl + need(rel));
+          if (t + 1 <= g.T) wait_seen(prog + w + 1, clvl + need(rel), seen_cons);
         } else if (t + 1 - NW >= 1) {
-          wait_smem(prog + w + 1, (t + 1 - NW) * BIG + fin);
+          wait_seen(prog + w + 1, (t + 1 - NW) * BIG + fin, seen_cons);
         }
       }
       PCOT_PROF(3);
