@@ -290,11 +290,11 @@ def main():
             "bytes_per_update": 16.0 / args.bt, "kernel_share_of_step": kernel_ms / ms if ms else None,
             "dram_bytes_per_update": (traffic["bytes_per_launch"] / (cells * args.bt)) if traffic else None}
 
-    # the same kernel at shallower temporal depths (one warm + one timed step
+    # the same kernel at other temporal depths (one warm + one timed step
     # each, after the timed region): the throughput / HBM-fraction trade-off
     depths = []
     if world == 1 and not args.no_depth_sweep:
-        for bt in (4, 5):
+        for bt in (4, 5, 8):
             if bt == args.bt:
                 continue
             S.bt = bt

@@ -29,6 +29,10 @@ namespace {
 
 constexpr int kPF = 8;  // TMA ring depth (rows in flight)
 
+#ifndef PCOT_S2_PFE
+#define PCOT_S2_PFE 2  // edge-exchange loads issued this many levels ahead of use
+#endif
+
 struct S2Args {
   const double* in;
   double* out;
@@ -80,9 +84,10 @@ struct EdgeLayout {
 };
 
 template <int BT, int C, int NT, int MASK, bool HOLD, bool XS, int P>
-PCOT_DEV void s2d5_iter(Regs<BT, C>& R, const double* __restrict__ ring_row, int k, int par,
-                        double* __restrict__ edge, int warp, int lane, const S2Args& a,
-                        int64_t cb, int r0, int r1, unsigned smask, unsigned cmask) {
+PCOT_DEV void s2d5_iter(Regs<BT, C>& R, const double* __restrict__ ring_row, uint64_t* bar,
+                        uint32_t phase, int k, int par, double* __restrict__ edge, int warp,
+                        int lane, const S2Args& a, int64_t cb, int r0, int r1, unsigned smask,
+                        unsigned cmask) {
   constexpr int NW = NT / 32;
   constexpr int SHIFT = 0;  // window start is even for every depth (see s2d5_tile)
   constexpr int EP = EdgeLayout<BT, NT, XS>::kPerPar;
@@ -92,6 +97,19 @@ PCOT_DEV void s2d5_iter(Regs<BT, C>& R, const double* __restrict__ ring_row, int
   // XS layout: [level][L=0 / R=1][NT+2], thread t at index t+1
   auto xs_l = [&](double* base, int L) { return base + (L * 2 + 0) * (NT + 2); };
   auto xs_r = [&](double* base, int L) { return base + (L * 2 + 1) * (NT + 2); };
+  // XS: the neighbours' edges were published in the previous iteration, so
+  // their loads need not wait for this row's TMA, nor sit on the level chain:
+  // they are issued kPFE levels ahead of use (levels 0..kPFE-1 before the wait).
+  constexpr int kPFE = PCOT_S2_PFE;
+  double Wp[BT], Ep[BT];
+  if constexpr (XS) {
+#pragma unroll
+    for (int L = 0; L < (kPFE < BT ? kPFE : BT); ++L) {
+      Wp[L] = xs_r(const_cast<double*>(eprev), L)[tid];
+      Ep[L] = xs_l(const_cast<double*>(eprev), L)[tid + 2];
+    }
+  }
+  mbar_wait(bar, phase);
   // ---- level 0: input row k
   {
     constexpr int s = smod3(P);
@@ -122,8 +140,12 @@ PCOT_DEV void s2d5_iter(Regs<BT, C>& R, const double* __restrict__ ring_row, int
     const double* bot = R.v[L][sb];
     double W, E;
     if constexpr (XS) {
-      W = xs_r(const_cast<double*>(eprev), L)[tid];
-      E = xs_l(const_cast<double*>(eprev), L)[tid + 2];
+      if (L + kPFE < BT) {
+        Wp[L + kPFE < BT ? L + kPFE : 0] = xs_r(const_cast<double*>(eprev), L + kPFE)[tid];
+        Ep[L + kPFE < BT ? L + kPFE : 0] = xs_l(const_cast<double*>(eprev), L + kPFE)[tid + 2];
+      }
+      W = Wp[L];
+      E = Ep[L];
     } else {
       W = __shfl_up_sync(0xffffffffu, mid[C - 1], 1);
       E = __shfl_down_sync(0xffffffffu, mid[0], 1);
@@ -171,6 +193,9 @@ PCOT_DEV void s2d5_iter(Regs<BT, C>& R, const double* __restrict__ ring_row, int
       if (SHIFT == 0 && C % 2 == 0 && smask == (1u << C) - 1u) {
 #pragma unroll
         for (int c = 0; c < C; c += 2)
+#ifdef PCOT_S2_EXP_NOSTORE  // experiment: store only when the result is NaN
+          if (nv[c] != nv[c])
+#endif
           __stcs(reinterpret_cast<double2*>(dst + c), make_double2(nv[c], nv[c + 1]));
       } else if (smask != 0u && smask != (1u << C) - 1u) {
 #pragma unroll
@@ -219,7 +244,11 @@ PCOT_DEV void s2d5_tile(const S2Args& a, int strip, int chunk, double* ring, uin
     if (cb + c >= 1 && cb + c <= a.cols - 2) cmask |= 1u << c;
 
   auto issue = [&](int64_t it) {
+#ifdef PCOT_S2_EXP_NOLOAD  // experiment: every row from one L2-resident row
+    int64_t row = kstart + (it & 1);
+#else
     int64_t row = kstart + it;
+#endif
     row = row < a.load_lo ? a.load_lo : (row > a.load_hi ? a.load_hi : row);
     const int slot = int(it % kPF);
     mbar_arrive_expect_tx(&bars[slot], W_LOAD * 8);
@@ -243,9 +272,9 @@ PCOT_DEV void s2d5_tile(const S2Args& a, int strip, int chunk, double* ring, uin
   {                                                                                        \
     const int itp = it + P;                                                                \
     const int slot = itp % kPF;                                                            \
-    mbar_wait(&bars[slot], uint32_t((itp / kPF) & 1));                                     \
-    s2d5_iter<BT, C, NT, MASK, HOLD, XS, P>(R, ring + slot * W_LOAD, kstart + itp, itp & 1, \
-                                            edge, warp, lane, a, cb, r0, r1, smask, cmask); \
+    s2d5_iter<BT, C, NT, MASK, HOLD, XS, P>(R, ring + slot * W_LOAD, &bars[slot],            \
+                                            uint32_t((itp / kPF) & 1), kstart + itp, itp & 1, \
+                                            edge, warp, lane, a, cb, r0, r1, smask, cmask);   \
     __syncthreads();                                                                       \
     if (tid == 0 && itp + kPF < niter) issue(itp + kPF);                                   \
   }
@@ -352,7 +381,7 @@ cudaError_t launch_bt(const S2Args& a, int ring_hold, int rows, int variant, cud
     if (int64_t(rows) * a.cols <= (int64_t(1) << 24))
       variant = 9;  // small grids: narrow strips so the launch fills 148 SMs
     else
-      variant = BT <= 5 ? 6 : BT == 6 ? 11 : 4;
+      variant = BT <= 4 ? 6 : BT == 6 ? 12 : 4;
   }
   switch (variant) {
     case 1: return launch_cfg<BT, 2, 256, 2, false>(a, ring_hold, rows, s);
@@ -366,6 +395,12 @@ cudaError_t launch_bt(const S2Args& a, int ring_hold, int rows, int variant, cud
     case 9: return launch_cfg<BT, 2, 64, 8, true>(a, ring_hold, rows, s);
     case 10: return launch_cfg<BT, 4, 64, 6, true>(a, ring_hold, rows, s);
     case 11: return launch_cfg<BT, 4, 96, 4, true>(a, ring_hold, rows, s);
+    // six columns per thread: 1/3 less edge exchange per update, and the
+    // 48-B per-thread stride makes the level-0 LDS.128 bank-conflict free
+    case 12: return launch_cfg<BT, 6, 64, 3, true>(a, ring_hold, rows, s);
+    case 13: return launch_cfg<BT, 6, 64, 4, true>(a, ring_hold, rows, s);
+    case 14: return launch_cfg<BT, 6, 128, 2, true>(a, ring_hold, rows, s);
+    case 15: return launch_cfg<BT, 6, 32, 8, true>(a, ring_hold, rows, s);
 
     default: return launch_cfg<BT, 4, 128, 2, false>(a, ring_hold, rows, s);
   }
@@ -403,6 +438,10 @@ cudaError_t s2d5_advance(const Slab2D& in, const Slab2D& out, int64_t g0, int64_
     variant = v ? std::atoi(v) : -1;  // -1: automatic per depth
   }
   const int rows = row_hi - row_lo;
+#ifdef PCOT_S2_DEV_BT  // development: instantiate one depth only (fast SASS checks)
+  return bt == PCOT_S2_DEV_BT ? launch_bt<PCOT_S2_DEV_BT>(a, ring_hold, rows, variant, stream)
+                              : cudaErrorInvalidValue;
+#else
   switch (bt) {
     case 1: return launch_bt<1>(a, ring_hold, rows, variant, stream);
     case 2: return launch_bt<2>(a, ring_hold, rows, variant, stream);
@@ -413,6 +452,7 @@ cudaError_t s2d5_advance(const Slab2D& in, const Slab2D& out, int64_t g0, int64_
     case 7: return launch_bt<7>(a, ring_hold, rows, variant, stream);
     default: return launch_bt<8>(a, ring_hold, rows, variant, stream);
   }
+#endif
 }
 
 }  // namespace pcotgpu

@@ -385,6 +385,26 @@ PCOT_DEV void s3v2_iter(Regs3v2<BT, G>& R, const double* __restrict__ ring, int 
   const double* p2 = ring + ((k % PF + PF) % PF) * SLOT + tb;
   const double* eprev = edge + (par ^ 1) * Edge3v2<BT, G>::kPerPar;
   double* ecur = edge + par * Edge3v2<BT, G>::kPerPar;
+  // Warp-edge rows of levels >= 1 were published in the previous iteration:
+  // load them kPFE levels ahead of use (the first ones before level 0), so the
+  // shared-memory latency is off the level chain (the compiler cannot hoist an
+  // eprev load above this iteration's ecur stores itself).
+  constexpr int LVp = Edge3v2<BT, G>::LV;
+  constexpr int kPFE = 2;
+  double upP[LVp][C], dnP[LVp][C];
+  auto prefetch = [&](const int L) {  // level L >= 1
+    if (L >= 1 && L < BT) {
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        upP[L >= 1 && L < BT ? L - 1 : 0][c] =
+            eprev[(warp + 0) * EW + ((1 * LVp + (L - 1)) * 32 + lane) * C + c];
+        dnP[L >= 1 && L < BT ? L - 1 : 0][c] =
+            eprev[(warp + 2) * EW + ((0 * LVp + (L - 1)) * 32 + lane) * C + c];
+      }
+    }
+  };
+#pragma unroll
+  for (int L = 1; L <= kPFE; ++L) prefetch(L);
   // ---- level 0 -> 1, plane k-1
   {
     const int rho = k - 1;
@@ -498,18 +518,16 @@ PCOT_DEV void s3v2_iter(Regs3v2<BT, G>& R, const double* __restrict__ ring, int 
     const double(*mid)[C] = R.v[L - 1][sm];
     double nv[RJ][C];
     const bool ringp = rho < 1 || rho > a.n - 2;
+    prefetch(L + kPFE);
     if (ringp) {
 #pragma unroll
       for (int r = 0; r < RJ; ++r)
 #pragma unroll
         for (int c = 0; c < C; ++c) nv[r][c] = HOLD ? mid[r][c] : 0.0;
     } else {
-      double up[C], dn[C];
-#pragma unroll
-      for (int c = 0; c < C; ++c) {  // padded: warp 0 / NW-1 read pad rows (halo cells)
-        up[c] = eprev[(warp + 0) * EW + ((1 * LV + (L - 1)) * 32 + lane) * C + c];
-        dn[c] = eprev[(warp + 2) * EW + ((0 * LV + (L - 1)) * 32 + lane) * C + c];
-      }
+      // padded: warp 0 / NW-1 read pad rows (halo cells)
+      const double* up = upP[L - 1];
+      const double* dn = dnP[L - 1];
 #pragma unroll
       for (int r = 0; r < RJ; ++r) {
         const double W = __shfl_up_sync(0xffffffffu, mid[r][C - 1], 1);

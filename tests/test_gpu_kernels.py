@@ -92,9 +92,10 @@ def test_s3d7_variants_bit_exact(variant):
     assert p.returncode == 0 and "ok" in p.stdout, p.stdout + p.stderr
 
 
-@pytest.mark.parametrize("variant", [0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11])
+@pytest.mark.parametrize("variant", list(range(16)))
 def test_s2d5_variants_bit_exact(variant, monkeypatch):
-    """Every compiled (C, NT, MINB) variant of the 2-D kernel, all depths."""
+    """Every compiled (C, NT, MINB) variant of the 2-D kernel (12-15: six
+    columns per thread), all depths, zero ring (jacobi2d) and held ring (heat2d)."""
     import subprocess
     import sys
 
@@ -107,6 +108,12 @@ def test_s2d5_variants_bit_exact(variant, monkeypatch):
         "        ex.run('slt', [bt, 8, 8], skip_checksum=True)\n"
         "        out = ex.array_data('Out')\n"
         "        assert np.array_equal(out.view(np.uint64), want.view(np.uint64)), bt\n"
+        "want = O.reference_output('heat2d_hold', {'T': 19, 'N': 301})\n"
+        "with P.GpuExecutor(O.kernel_path('heat2d_hold'), {'T': 19, 'N': 301}) as ex:\n"
+        "    for bt in range(1, 9):\n"
+        "        ex.run('cot', [bt, 8, 8], skip_checksum=True)\n"
+        "        out = ex.array_data('Out')\n"
+        "        assert np.array_equal(out.view(np.uint64), want.view(np.uint64)), ('hold', bt)\n"
         "print('ok')\n")
     env = dict(**__import__("os").environ, PCOTGPU_S2D5_VARIANT=str(variant))
     p = subprocess.run([sys.executable, "-c", code], cwd=O.REPO, env=env, capture_output=True,
