@@ -5,10 +5,14 @@
 // tcgen05 has no f64 kind (CUDA 12.9 tcgen05_mma.h), so the fp64 tensor path
 // on sm_100a is warp-level mma.sync ... f64 (SASS: DMMA.8x8x4).
 //
-// CTA tile 128x128x16, 8 warps (2 x 4), warp tile 64x32 = 8x4 DMMA tiles;
-// 4-stage cp.async (LDGSTS) pipeline; shared-memory pitches chosen so every
-// 64-bit fragment load is bank-conflict free (pitch = 4 mod 16 doubles).
+// CTA tile 128x128xBK, WM x WN warps, warp tile (128/WM) x (128/WN) of 8x8
+// DMMA tiles; STAGES-deep cp.async (LDGSTS) pipeline; shared-memory pitches
+// chosen so every 64-bit fragment load is bank-conflict free (pitch = 4 mod
+// 16 doubles).  Default: 4 x 4 warps (32x32 warp tiles), BK 32, 3 stages;
+// PCOTGPU_DGEMM_VARIANT selects another (tools/kbench.py gemm).
 // Tile order: lexicographic or Morton (the COT-style recursive order).
+#include <cstdlib>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -16,12 +20,19 @@ namespace pcotgpu {
 
 namespace {
 
-constexpr int BM = 128, BN = 128, BK = 16, STAGES = 4;
-constexpr int APITCH = BK + 4;   // A stored [m][k]
-constexpr int BPITCH = BN + 4;   // B stored [k][n]
-constexpr int A_STAGE = BM * APITCH;
-constexpr int B_STAGE = BK * BPITCH;
-constexpr int NTHR = 256;
+constexpr int BM = 128, BN = 128;
+
+template <int WM_, int WN_, int BK_, int STAGES_>
+struct GemmCfg {
+  static constexpr int WM = WM_, WN = WN_, BK = BK_, STAGES = STAGES_;
+  static constexpr int NTHR = WM * WN * 32;
+  static constexpr int TM = BM / WM / 8, TN = BN / WN / 8;  // DMMA tiles per warp
+  static constexpr int APITCH = BK + 4;  // A stored [m][k]
+  static constexpr int BPITCH = BN + 4;  // B stored [k][n]
+  static constexpr int A_STAGE = BM * APITCH;
+  static constexpr int B_STAGE = BK * BPITCH;
+  static constexpr size_t SMEM = size_t(STAGES) * (A_STAGE + B_STAGE) * sizeof(double);
+};
 
 PCOT_DEV void cp_async16(void* smem, const void* gmem) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem)), "l"(gmem));
@@ -38,10 +49,14 @@ PCOT_DEV void dmma(double (&d)[2], double a, double b) {
                : "d"(a), "d"(b));
 }
 
-__global__ void __launch_bounds__(NTHR, 1)
+template <class G>
+__global__ void __launch_bounds__(G::NTHR, 1)
     dgemm_kernel(const double* __restrict__ A, const double* __restrict__ B,
                  double* __restrict__ C, int n, int64_t ld, int order, int tiles_m,
                  int tiles_n) {
+  constexpr int BK = G::BK, STAGES = G::STAGES, NTHR = G::NTHR, TM = G::TM, TN = G::TN;
+  constexpr int APITCH = G::APITCH, BPITCH = G::BPITCH, A_STAGE = G::A_STAGE,
+                B_STAGE = G::B_STAGE;
   extern __shared__ __align__(128) double sm[];
   double* sA = sm;
   double* sB = sm + STAGES * A_STAGE;
@@ -60,7 +75,7 @@ __global__ void __launch_bounds__(NTHR, 1)
     if (tm >= tiles_m || tn >= tiles_n) return;
   }
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int wm = warp >> 2, wn = warp & 3;  // 2 x 4 warps
+  const int wm = warp / G::WN, wn = warp % G::WN;
   const int g = lane >> 2, q = lane & 3;
   const int64_t row0 = int64_t(tm) * BM, col0 = int64_t(tn) * BN;
   const int nk = (n + BK - 1) / BK;
@@ -69,10 +84,11 @@ __global__ void __launch_bounds__(NTHR, 1)
     const int64_t k0 = int64_t(kt) * BK;
     double* a = sA + st * A_STAGE;
     double* b = sB + st * B_STAGE;
+    constexpr int KC = BK / 2;  // 16-B chunks per A row
 #pragma unroll
-    for (int r = 0; r < 4; ++r) {  // A: 128 rows x 8 chunks of 16 B
+    for (int r = 0; r < BM * KC / NTHR; ++r) {  // A: 128 rows x KC chunks of 16 B
       const int idx = tid + r * NTHR;
-      const int m = idx >> 3, kc = (idx & 7) * 2;
+      const int m = idx / KC, kc = (idx % KC) * 2;
       const int64_t gr = row0 + m, gk = k0 + kc;
       double* dst = a + m * APITCH + kc;
       if (gr < n && gk + 1 < n)
@@ -83,7 +99,7 @@ __global__ void __launch_bounds__(NTHR, 1)
       }
     }
 #pragma unroll
-    for (int r = 0; r < 4; ++r) {  // B: 16 rows x 64 chunks
+    for (int r = 0; r < BK * 64 / NTHR; ++r) {  // B: BK rows x 64 chunks
       const int idx = tid + r * NTHR;
       const int kk = idx >> 6, nc = (idx & 63) * 2;
       const int64_t gk = k0 + kk, gc = col0 + nc;
@@ -97,11 +113,11 @@ __global__ void __launch_bounds__(NTHR, 1)
     }
   };
 
-  double acc[8][4][2];
+  double acc[TM][TN][2];
 #pragma unroll
-  for (int i = 0; i < 8; ++i)
+  for (int i = 0; i < TM; ++i)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    for (int j = 0; j < TN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
 #pragma unroll
   for (int s = 0; s < STAGES - 1; ++s) {
@@ -116,30 +132,30 @@ __global__ void __launch_bounds__(NTHR, 1)
       if (nxt < nk) load_stage(nxt, nxt % STAGES);
       cp_commit();
     }
-    const double* a = sA + (kt % STAGES) * A_STAGE + (wm * 64 + g) * APITCH + q;
-    const double* b = sB + (kt % STAGES) * B_STAGE + q * BPITCH + wn * 32 + g;
+    const double* a = sA + (kt % STAGES) * A_STAGE + (wm * TM * 8 + g) * APITCH + q;
+    const double* b = sB + (kt % STAGES) * B_STAGE + q * BPITCH + wn * TN * 8 + g;
 #pragma unroll
     for (int ks = 0; ks < BK / 4; ++ks) {
-      double af[8], bf[4];
+      double af[TM], bf[TN];
 #pragma unroll
-      for (int i = 0; i < 8; ++i) af[i] = a[i * 8 * APITCH + ks * 4];
+      for (int i = 0; i < TM; ++i) af[i] = a[i * 8 * APITCH + ks * 4];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) bf[j] = b[ks * 4 * BPITCH + j * 8];
+      for (int j = 0; j < TN; ++j) bf[j] = b[ks * 4 * BPITCH + j * 8];
 #pragma unroll
-      for (int i = 0; i < 8; ++i)
+      for (int i = 0; i < TM; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) dmma(acc[i][j], af[i], bf[j]);
+        for (int j = 0; j < TN; ++j) dmma(acc[i][j], af[i], bf[j]);
     }
   }
   cp_wait<0>();
   // epilogue: C[g][2q..2q+1] of every 8x8 tile
 #pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    const int64_t r = row0 + wm * 64 + i * 8 + g;
+  for (int i = 0; i < TM; ++i) {
+    const int64_t r = row0 + wm * TM * 8 + i * 8 + g;
     if (r >= n) continue;
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int64_t c = col0 + wn * 32 + j * 8 + 2 * q;
+    for (int j = 0; j < TN; ++j) {
+      const int64_t c = col0 + wn * TN * 8 + j * 8 + 2 * q;
       if (c + 1 < n) {
         *reinterpret_cast<double2*>(C + r * ld + c) = make_double2(acc[i][j][0], acc[i][j][1]);
       } else if (c < n) {
@@ -157,6 +173,21 @@ __global__ void affine_kernel(const double* __restrict__ x, double* __restrict__
 
 }  // namespace
 
+template <class G>
+cudaError_t launch_gemm(const double* A, const double* B, double* C, int64_t n, int64_t ld,
+                        int order, int tiles_m, int tiles_n, int grid, cudaStream_t stream) {
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(dgemm_kernel<G>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, int(G::SMEM));
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  dgemm_kernel<G><<<grid, G::NTHR, G::SMEM, stream>>>(A, B, C, int(n), ld, order, tiles_m, tiles_n);
+  count_launch();
+  return cudaGetLastError();
+}
+
 cudaError_t dgemm_nn(const double* A, const double* B, double* C, int64_t n, int64_t ld,
                      int order, cudaStream_t stream) {
   if (n <= 0) return cudaSuccess;
@@ -170,13 +201,24 @@ cudaError_t dgemm_nn(const double* A, const double* B, double* C, int64_t n, int
     while (side < tiles_m || side < tiles_n) side <<= 1;
     grid = side * side;
   }
-  const size_t smem = size_t(STAGES) * (A_STAGE + B_STAGE) * sizeof(double);
-  cudaError_t e =
-      cudaFuncSetAttribute(dgemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-  if (e != cudaSuccess) return e;
-  dgemm_kernel<<<grid, NTHR, smem, stream>>>(A, B, C, int(n), ld, order, tiles_m, tiles_n);
-  count_launch();
-  return cudaGetLastError();
+  static int variant = -2;
+  if (variant == -2) {
+    const char* v = std::getenv("PCOTGPU_DGEMM_VARIANT");
+    variant = v ? std::atoi(v) : 0;  // 0: default
+  }
+  // measured on the B200 at N=4096 (tools/kbench.py gemm; profiles/dgemm_r01.md)
+  switch (variant) {
+    case 1: return launch_gemm<GemmCfg<2, 4, 16, 4>>(A, B, C, n, ld, order, tiles_m, tiles_n, grid, stream);  // 28.2 TF/s
+    case 2: return launch_gemm<GemmCfg<4, 4, 16, 4>>(A, B, C, n, ld, order, tiles_m, tiles_n, grid, stream);  // 29.3
+    case 3: return launch_gemm<GemmCfg<2, 4, 32, 3>>(A, B, C, n, ld, order, tiles_m, tiles_n, grid, stream);  // 29.4
+    case 4: return launch_gemm<GemmCfg<4, 2, 16, 4>>(A, B, C, n, ld, order, tiles_m, tiles_n, grid, stream);  // 28.2
+    case 5: return launch_gemm<GemmCfg<2, 4, 16, 6>>(A, B, C, n, ld, order, tiles_m, tiles_n, grid, stream);  // 30.3
+    case 6: return launch_gemm<GemmCfg<4, 4, 16, 6>>(A, B, C, n, ld, order, tiles_m, tiles_n, grid, stream);  // 30.0
+    case 7: return launch_gemm<GemmCfg<4, 4, 24, 4>>(A, B, C, n, ld, order, tiles_m, tiles_n, grid, stream);  // 29.1
+    case 8: return launch_gemm<GemmCfg<2, 4, 24, 4>>(A, B, C, n, ld, order, tiles_m, tiles_n, grid, stream);  // 28.5
+    // default: 16 warps (32x32 warp tiles), BK 32, 3 stages: 30.5 TF/s
+    default: return launch_gemm<GemmCfg<4, 4, 32, 3>>(A, B, C, n, ld, order, tiles_m, tiles_n, grid, stream);
+  }
 }
 
 cudaError_t affine_2x_minus_1(const double* x, double* y, int64_t count, cudaStream_t stream) {
