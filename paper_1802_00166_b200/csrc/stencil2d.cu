@@ -265,24 +265,37 @@ PCOT_DEV void s2d5_tile(const S2Args& a, int strip, int chunk, double* ring, uin
 #pragma unroll
       for (int c = 0; c < C; ++c) R.v[L][s][c] = 0.0;
 
+  // Row-edge chunks need the row mask only while some level's row is on or
+  // outside the ring: input rows k with every level's row k-1-L (L < BT) in
+  // [1, nrows-2] (global) run the unmasked body.
+  const int64_t k_safe_lo = 1 - a.g0 + BT, k_safe_hi = a.nrows - 1 - a.g0;
+  // The TMA refill rotates over the warps (lane 0): the ~30 issue
+  // instructions would otherwise make warp 0 the last to reach every barrier.
+  constexpr int NW = NT / 32;
   // Every warp waits on the row's mbarrier itself (measured faster than one
   // waiter + the barrier: the try_wait latency then overlaps across warps).
+#define PCOT_S2_STEP(M, P)                                                                       \
+  {                                                                                              \
+    const int itp = it + P;                                                                      \
+    const int slot = itp % kPF;                                                                  \
+    s2d5_iter<BT, C, NT, M, HOLD, XS, P>(R, ring + slot * W_LOAD, &bars[slot],                   \
+                                         uint32_t((itp / kPF) & 1), kstart + itp, itp & 1, edge, \
+                                         warp, lane, a, cb, r0, r1, smask, cmask);               \
+    __syncthreads();                                                                             \
+    if (lane == 0 && warp == itp % NW && itp + kPF < niter) issue(itp + kPF);                    \
+  }
   for (int it = 0; it < niter; it += 3) {
-#define PCOT_S2_STEP(P)                                                                    \
-  {                                                                                        \
-    const int itp = it + P;                                                                \
-    const int slot = itp % kPF;                                                            \
-    s2d5_iter<BT, C, NT, MASK, HOLD, XS, P>(R, ring + slot * W_LOAD, &bars[slot],            \
-                                            uint32_t((itp / kPF) & 1), kstart + itp, itp & 1, \
-                                            edge, warp, lane, a, cb, r0, r1, smask, cmask);   \
-    __syncthreads();                                                                       \
-    if (tid == 0 && itp + kPF < niter) issue(itp + kPF);                                   \
+    if ((MASK & 2) && !(kstart + it >= k_safe_lo && kstart + it + 2 <= k_safe_hi)) {
+      PCOT_S2_STEP(MASK, 0)
+      PCOT_S2_STEP(MASK, 1)
+      PCOT_S2_STEP(MASK, 2)
+    } else {
+      PCOT_S2_STEP(MASK & 1, 0)
+      PCOT_S2_STEP(MASK & 1, 1)
+      PCOT_S2_STEP(MASK & 1, 2)
+    }
   }
-    PCOT_S2_STEP(0)
-    PCOT_S2_STEP(1)
-    PCOT_S2_STEP(2)
 #undef PCOT_S2_STEP
-  }
 }
 
 template <int MINB>
