@@ -336,20 +336,33 @@ __global__ void __launch_bounds__(NT, MINB) s2d5_kernel(S2Args a) {
 
 // Pick the chunk height so the grid fills whole waves of resident CTAs:
 // minimise waves * (H + 2*BT + 2) (time ~ rounds x rows streamed per tile).
+// Tall tiles in few waves measured up to 1.6x slower than many waves of
+// ~250-500-row tiles on the 32768^2 grid (profiles/s2d5_r01b.md), so chunks
+// taller than 512 rows are re-chosen around 384 rows.
 void size_grid(S2Args& a, int bt, int rows, int slots) {
   const int hmin = 16 * bt > 48 ? 16 * bt : 48;
-  int best_n = 1;
-  double best = 1e300;
+  auto pick = [&](int lo, int hi) {
+    int best_n = lo;
+    double best = 1e300;
+    for (int nc = lo; nc <= hi; ++nc) {
+      const int H = (rows + nc - 1) / nc;
+      const int64_t tiles = int64_t(a.nstrips) * nc;
+      const int64_t waves = (tiles + slots - 1) / slots;
+      const double cost = double(waves) * (H + 2 * bt + 2);
+      if (cost < best * 0.999) best = cost, best_n = nc;
+    }
+    return best_n;
+  };
   const int maxc = rows / hmin > 1 ? rows / hmin : 1;
-  for (int nc = 1; nc <= maxc; ++nc) {
-    const int H = (rows + nc - 1) / nc;
-    const int64_t tiles = int64_t(a.nstrips) * nc;
-    const int64_t waves = (tiles + slots - 1) / slots;
-    const double cost = double(waves) * (H + 2 * bt + 2);
-    if (cost < best * 0.999) best = cost, best_n = nc;
+  int nc = pick(1, maxc);
+  if ((rows + nc - 1) / nc > 512) {
+    const int mid = rows / 384 > 1 ? rows / 384 : 1;
+    const int lo = mid * 3 / 4 > 1 ? mid * 3 / 4 : 1;
+    const int hi = mid * 4 / 3 < maxc ? mid * 4 / 3 : maxc;
+    nc = pick(lo, hi > lo ? hi : lo);
   }
-  a.nchunks = best_n;
-  a.H = (rows + best_n - 1) / best_n;
+  a.nchunks = nc;
+  a.H = (rows + nc - 1) / nc;
 }
 
 template <int BT, int C, int NT, int MINB, bool XS>
@@ -373,6 +386,15 @@ cudaError_t launch_cfg(S2Args a, int ring_hold, int rows, cudaStream_t stream) {
   a.w_out = NT * C - 2 * BT;
   a.nstrips = int((a.cols + (BT & 1) + a.w_out - 1) / a.w_out);
   size_grid(a, BT, rows, sl);
+  static int force_chunks = -1;  // PCOTGPU_S2D5_CHUNKS: tuning override of the row chunking
+  if (force_chunks < 0) {
+    const char* v = std::getenv("PCOTGPU_S2D5_CHUNKS");
+    force_chunks = v ? std::atoi(v) : 0;
+  }
+  if (force_chunks > 0 && force_chunks <= rows) {
+    a.nchunks = force_chunks;
+    a.H = (rows + force_chunks - 1) / force_chunks;
+  }
   int grid;
   if (a.order == kOrderMorton) {
     int side = 1;
