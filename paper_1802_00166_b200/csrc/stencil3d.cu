@@ -30,6 +30,16 @@ namespace pcotgpu {
 
 namespace {
 
+// PCOTGPU_S3D7_CHUNKS: tuning override of the plane chunking (tools/kbench.py s3d7)
+int forced_chunks() {
+  static int fc = -1;
+  if (fc < 0) {
+    const char* v = std::getenv("PCOTGPU_S3D7_CHUNKS");
+    fc = v ? std::atoi(v) : 0;
+  }
+  return fc;
+}
+
 template <int C_, int RJ_, int NW_, int MINB_, int PF_>
 struct Geo {
   static constexpr int C = C_, RJ = RJ_, NW = NW_, MINB = MINB_, PF = PF_;
@@ -315,6 +325,10 @@ cudaError_t launch3(S3Args a, cudaStream_t stream) {
   }
   a.nchunks = best;
   a.H = (a.n + best - 1) / best;
+  if (const int fc = forced_chunks(); fc > 0 && fc <= a.n) {
+    a.nchunks = fc;
+    a.H = (a.n + fc - 1) / fc;
+  }
   int grid;
   if (a.order == kOrderLex) {
     grid = a.nk * a.nj * a.nchunks;
@@ -754,6 +768,10 @@ cudaError_t launch3v2(S3Args a, cudaStream_t stream) {
   }
   a.nchunks = best;
   a.H = (a.n + best - 1) / best;
+  if (const int fc = forced_chunks(); fc > 0 && fc <= a.n) {
+    a.nchunks = fc;
+    a.H = (a.n + fc - 1) / fc;
+  }
   int grid;
   if (a.order == kOrderLex) {
     grid = a.nk * a.nj * a.nchunks;
