@@ -73,6 +73,18 @@ PCOT_DEV void tma_load_3d(void* dst, const void* tmap, int c0, int c1, int c2, u
       : "memory");
 }
 
+// ---------------------------------------------------------------- programmatic dependent launch
+// A grid launched with cudaLaunchAttributeProgrammaticStreamSerialization may
+// start while the previous kernel in the stream drains; it must not touch
+// global memory before griddep_wait() (which returns once that kernel has
+// completed and its writes are visible; a no-op for a plain launch).
+PCOT_DEV void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+// Lets the next PDL kernel in the stream begin launching its CTAs (they wait in
+// griddep_wait until this grid completes).
+PCOT_DEV void griddep_launch_dependents() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 // ---------------------------------------------------------------- acquire/release flags
 PCOT_DEV int ld_acquire(const int* p) {
   int v;

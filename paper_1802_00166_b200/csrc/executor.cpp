@@ -242,8 +242,9 @@ struct GpuExecutor::Impl {
 
   int run_stencil2d(const TileOrder& o) {
     // default depth: 6 for HBM-streaming grids (power-capped optimum, bench.py),
-    // 4 for L2-resident ones (<= 2^24 cells: warm-up rows dominate deeper blocks)
-    const int bt = pick_bt(o, env_int("PCOTGPU_BT2D", n * n <= (int64_t(1) << 24) ? 4 : 6),
+    // 8 for L2-resident ones (<= 2^24 cells: the fewest launches of short
+    // chunks; 2048^2 T=256: bt=8 907, bt=6 790, bt=4 648-800 GUpd/s)
+    const int bt = pick_bt(o, env_int("PCOTGPU_BT2D", n * n <= (int64_t(1) << 24) ? 8 : 6),
                            s2d5_max_bt());
     const int order = o.scheme == Scheme::Cot ? kOrderMorton : kOrderLex;
     ck(copy_rows(sg[0].origin, sg[0].ld, in[0].p, in_ld, n, n, stream), "copy_rows");

@@ -18,12 +18,23 @@
 //     shared-memory edge exchange across warps (one __syncthreads per row).
 // Operation order per point is the reference body's parse tree:
 //   0.2 * ((((c + (i-1,j)) + (i+1,j)) + (i,j-1)) + (i,j+1)), no FMA.
+#include <cstdio>
 #include <cstdlib>
 
 #include "common.cuh"
 #include "kernels.h"
 
 namespace pcotgpu {
+
+// PCOTGPU_PDL=0 turns programmatic dependent launch off (A/B measurements).
+bool pdl_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = std::getenv("PCOTGPU_PDL");
+    v = e && e[0] == '0' ? 0 : 1;
+  }
+  return v == 1;
+}
 
 namespace {
 
@@ -318,6 +329,11 @@ __global__ void __launch_bounds__(NT, MINB) s2d5_kernel(S2Args a) {
     fence_mbar_init();
   }
   __syncthreads();
+  // PDL: the prologue above overlaps the previous launch's tail; its output
+  // (this launch's input) and its input (this launch's output) are safe after
+  // the wait.  Dependents may then start launching into freed slots.
+  griddep_wait();
+  griddep_launch_dependents();
   const int64_t c0 = int64_t(strip) * a.w_out - (BT & 1);
   const int64_t r0 = a.row_lo + int64_t(chunk) * a.H;
   const int64_t r1 = r0 + a.H < a.row_hi ? r0 + a.H : a.row_hi;
@@ -338,9 +354,13 @@ __global__ void __launch_bounds__(NT, MINB) s2d5_kernel(S2Args a) {
 // minimise waves * (H + 2*BT + 2) (time ~ rounds x rows streamed per tile).
 // Tall tiles in few waves measured up to 1.6x slower than many waves of
 // ~250-500-row tiles on the 32768^2 grid (profiles/s2d5_r01b.md), so chunks
-// taller than 512 rows are re-chosen around 384 rows.
+// taller than 512 rows are re-chosen around 384 rows.  Grids that cannot fill
+// every resident slot with one wave of such tiles (L2-resident grids, e.g.
+// 2048^2) are latency-bound per row, so there the chunks shrink down to
+// 2*BT+16 rows until the wave is full (2048^2, bt=4: 64-row -> 32-row tiles,
+// 597 -> 731 GUpd/s, tools/cfg0_sweep.sh).
 void size_grid(S2Args& a, int bt, int rows, int slots) {
-  const int hmin = 16 * bt > 48 ? 16 * bt : 48;
+  const int hmin = 2 * bt + 16;
   auto pick = [&](int lo, int hi) {
     int best_n = lo;
     double best = 1e300;
@@ -403,9 +423,26 @@ cudaError_t launch_cfg(S2Args a, int ring_hold, int rows, cudaStream_t stream) {
   } else {
     grid = a.nstrips * a.nchunks;
   }
-  kern<<<grid, NT, smem, stream>>>(a);
+  static int dbg = -1;
+  if (dbg < 0) dbg = std::getenv("PCOTGPU_S2D5_DEBUG") ? 1 : 0;
+  if (dbg)
+    std::fprintf(stderr, "s2d5 bt=%d C=%d NT=%d slots=%d strips=%d chunks=%d H=%d grid=%d\n", BT, C,
+                 NT, sl, a.nstrips, a.nchunks, a.H, grid);
+  // Programmatic dependent launch: back-to-back depth blocks overlap one
+  // launch's drain with the next one's CTA launch and prologue.
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(NT);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, a);
   count_launch();
-  return cudaGetLastError();
+  return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 // Variant table: (C, NT, MINB).  Variant 0 is the default; PCOTGPU_S2D5_VARIANT
@@ -414,7 +451,8 @@ template <int BT>
 cudaError_t launch_bt(const S2Args& a, int ring_hold, int rows, int variant, cudaStream_t s) {
   if (variant < 0) {  // measured best per depth (tools/kbench.py s2d5; profiles/kbench_r01.md)
     if (int64_t(rows) * a.cols <= (int64_t(1) << 24))
-      variant = 9;  // small grids: narrow strips so the launch fills 148 SMs
+      variant = 8;  // small (L2-resident) grids: 128-thread strips, 4 CTAs/SM, short chunks
+                    // (2048^2 T=256 at bt=8: 907 GUpd/s; profiles/cfg0_r01.txt)
     else
       variant = BT <= 4 ? 6 : BT == 6 ? 12 : 4;
   }

@@ -28,6 +28,8 @@
 
 namespace pcotgpu {
 
+bool pdl_enabled();  // stencil2d.cu
+
 namespace {
 
 // PCOTGPU_S3D7_CHUNKS: tuning override of the plane chunking (tools/kbench.py s3d7)
@@ -707,6 +709,8 @@ __global__ void __launch_bounds__(G::NT, G::MINB)
     fence_mbar_init();
   }
   __syncthreads();
+  griddep_wait();  // PDL: no global access before the previous depth block completes
+  griddep_launch_dependents();
   const int k0 = tk * a.kout - (BT & 1), j0 = tj * a.jout;
   const bool edge_jk = (k0 - BT <= 0) || (k0 + a.kout + BT >= a.n - 1) || (j0 - BT <= 0) ||
                        (j0 + a.jout + BT >= a.n - 1);
@@ -783,9 +787,19 @@ cudaError_t launch3v2(S3Args a, cudaStream_t stream) {
   CUtensorMap tmap;
   cudaError_t e = encode_plane_map(&tmap, a, G::KL, G::JL);
   if (e != cudaSuccess) return e;
-  fn<<<grid, G::NT, smem, stream>>>(a, tmap);
+  cudaLaunchConfig_t cfg = {};  // programmatic dependent launch (see stencil2d.cu)
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(G::NT);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  e = cudaLaunchKernelEx(&cfg, fn, a, tmap);
   count_launch();
-  return cudaGetLastError();
+  return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 template <int BT, class G>

@@ -3,6 +3,7 @@
 
     python tools/kbench.py s2d5 [--rows R --cols C --bts 1,2,...]
     python tools/kbench.py s3d7 [--n 384 --bts 1,2,3,4]
+    python tools/kbench.py jac  [--n 2048 --T 256 --bts 2,4,6]   (executor, jacobi2d)
     python tools/kbench.py gs   [--n 4096 --T 64 --tiles 4x32x256,...]
     python tools/kbench.py gemm [--n 4096]
 """
@@ -82,6 +83,11 @@ def main():
         tiles = [[int(b), 8, 8, 8] for b in a.bts.split(",") if int(b) <= 4]
         for ms in executor(a, "heat3d_b", {"T": T, "N": n}, tiles):
             print("  GUpd/s %.1f" % (n ** 3 * T / ms / 1e6))
+    elif a.which == "jac":
+        n, T = a.n or 2048, a.T or 256
+        tiles = [[int(b), 8, 8] for b in a.bts.split(",")]
+        for ms in executor(a, "jacobi2d", {"T": T, "N": n}, tiles):
+            print("  GUpd/s %.1f" % (n * n * T / ms / 1e6))
     elif a.which == "gs":
         n, T = a.n or 4096, a.T or 64
         tiles = [[int(v) for v in t.split("x")] for t in (a.tiles or "4x32x256").split(",")]
