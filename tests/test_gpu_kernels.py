@@ -119,3 +119,32 @@ def test_s2d5_variants_bit_exact(variant, monkeypatch):
     p = subprocess.run([sys.executable, "-c", code], cwd=O.REPO, env=env, capture_output=True,
                        text=True, timeout=600)
     assert p.returncode == 0 and "ok" in p.stdout, p.stdout + p.stderr
+
+
+@pytest.mark.parametrize("env", [{}, {"PCOTGPU_PDL": "0"}, {"PCOTGPU_S2D5_CHUNKS": "1"},
+                                 {"PCOTGPU_S2D5_CHUNKS": "333", "PCOTGPU_S3D7_CHUNKS": "29"}])
+def test_launch_modes_bit_exact(env):
+    """Programmatic dependent launch on/off and extreme row chunkings leave every
+    bit unchanged: an L2-resident grid (short chunks filling the resident
+    slots), a multi-wave HBM-streaming grid (> 2^24 cells, 13 back-to-back
+    depth blocks) and the 3-D kernel."""
+    import subprocess
+    import sys
+
+    code = (
+        "import numpy as np, paper_1802_00166_b200 as P\n"
+        "from tests import oracle_ctypes as O\n"
+        "for k, prm, tiles in (('jacobi2d', {'T': 40, 'N': 2049}, ([8, 8, 8], [3, 8, 8])),\n"
+        "                      ('jacobi2d', {'T': 13, 'N': 4500}, ([6, 8, 8], [1, 8, 8])),\n"
+        "                      ('heat3d_b', {'T': 11, 'N': 97}, ([2, 8, 8, 8], [3, 8, 8, 8]))):\n"
+        "    want = O.reference_output(k, prm)\n"
+        "    with P.GpuExecutor(k, prm) as ex:\n"
+        "        for tile in tiles:\n"
+        "            ex.run('slt', tile, skip_checksum=True)\n"
+        "            out = ex.array_data('Out')\n"
+        "            assert np.array_equal(out.view(np.uint64), want.view(np.uint64)), (k, tile)\n"
+        "print('ok')\n")
+    e = dict(**__import__("os").environ, **env)
+    p = subprocess.run([sys.executable, "-c", code], cwd=O.REPO, env=e, capture_output=True,
+                       text=True, timeout=900)
+    assert p.returncode == 0 and "ok" in p.stdout, p.stdout + p.stderr
