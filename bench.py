@@ -213,6 +213,8 @@ def main():
     ap.add_argument("--bt", type=int, default=int(os.environ.get("PCOTGPU_BT2D", 6)))
     ap.add_argument("--scheme", default="slt", choices=["slt", "cot"])
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
+    ap.add_argument("--halo", default="nccl", choices=["nccl", "p2p"],
+                    help="N>1 halo exchange: NCCL send/recv (overlapped) or P2P stores fused into the kernel")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-depth-sweep", action="store_true")
@@ -234,7 +236,7 @@ def main():
         dist.init_process_group("nccl", device_id=dev)
     rows = args.rows if args.scaling == "weak" else args.rows // world
     S = ShardedStencil2D(rows, args.cols, args.T, args.bt, ring_hold=0,
-                         order=0 if args.scheme == "slt" else 1, device=dev)
+                         order=0 if args.scheme == "slt" else 1, device=dev, halo=args.halo)
     S.fill_init("F")
     S.snapshot_input()
     torch.cuda.synchronize()
@@ -337,7 +339,9 @@ def main():
                                    % (rows, args.cols, args.T),
                        "global_grid": [rows * world, args.cols], "T": args.T, "bt": args.bt,
                        "tile_order": args.scheme, "parallelism": "row-shard x%d" % world,
-                       "halo": "NCCL send/recv of bt rows every bt steps, overlapped" if world > 1 else None,
+                       "halo": (None if world == 1 else
+                                "NCCL send/recv of bt rows every bt steps, overlapped" if args.halo == "nccl" else
+                                "P2P stores of bt rows into the neighbours' ghost rows from the stencil kernel"),
                        "l2": "inputs larger than L2 (two %.1f GiB slabs per rank)" % (cells * 8 / 2**30)},
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
             "clocks": {"sm_mhz": cl["sm_mhz"], "sm_max_mhz": cl["sm_max_mhz"], "reasons": cl["reasons"]},

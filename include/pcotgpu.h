@@ -134,6 +134,17 @@ int pcotgpu_s2d5_layout(int64_t rows, int64_t cols, int64_t* ld, int64_t* ghost,
 int pcotgpu_s2d5_advance(const double* in_origin, double* out_origin, int64_t rows, int64_t cols,
                          int64_t g0, int64_t nrows_global, int bt, int ring_hold, int order,
                          int64_t row_lo, int64_t row_hi, void* stream);
+/* Same, with the halo exchange fused into the kernel (P2P stores over NVLink):
+ * owned output rows [0, mirror_rows) are also written to
+ * mirror_up + row*ld + col and rows [rows - mirror_rows, rows) to
+ * mirror_dn + row*ld + col, where mirror_up = upper neighbour's out origin +
+ * rows*ld (its ghost rows below) and mirror_dn = lower neighbour's out origin -
+ * rows*ld (its ghost rows above); NULL mirrors are skipped.  Replaces the
+ * NCCL send/recv of sharded.py's exchange; mirror_rows <= ghost rows. */
+int pcotgpu_s2d5_advance_p2p(const double* in_origin, double* out_origin, int64_t rows,
+                             int64_t cols, int64_t g0, int64_t nrows_global, int bt, int ring_hold,
+                             int order, int64_t row_lo, int64_t row_hi, double* mirror_up,
+                             double* mirror_dn, int64_t mirror_rows, void* stream);
 /* init_value(name, flat0 + r*cols + c) into a pitched block. */
 int pcotgpu_fill_init_value(double* dst, int64_t ld, int64_t nrows, int64_t ncols,
                             const char* name, uint64_t flat0, void* stream);

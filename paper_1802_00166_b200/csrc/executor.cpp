@@ -887,6 +887,14 @@ int pcotgpu_s2d5_layout(int64_t rows, int64_t cols, int64_t* ld, int64_t* ghost,
 int pcotgpu_s2d5_advance(const double* in_origin, double* out_origin, int64_t rows, int64_t cols,
                          int64_t g0, int64_t nrows_global, int bt, int ring_hold, int order,
                          int64_t row_lo, int64_t row_hi, void* stream) {
+  return pcotgpu_s2d5_advance_p2p(in_origin, out_origin, rows, cols, g0, nrows_global, bt,
+                                  ring_hold, order, row_lo, row_hi, nullptr, nullptr, 0, stream);
+}
+
+int pcotgpu_s2d5_advance_p2p(const double* in_origin, double* out_origin, int64_t rows,
+                             int64_t cols, int64_t g0, int64_t nrows_global, int bt, int ring_hold,
+                             int order, int64_t row_lo, int64_t row_hi, double* mirror_up,
+                             double* mirror_dn, int64_t mirror_rows, void* stream) {
   Slab2D a, b;
   int64_t ld = 0;
   pcotgpu_s2d5_layout(rows, cols, &ld, nullptr, nullptr, nullptr);
@@ -897,8 +905,11 @@ int pcotgpu_s2d5_advance(const double* in_origin, double* out_origin, int64_t ro
   a.cols = b.cols = cols;
   a.ghost = b.ghost = kGhost;
   a.padl = b.padl = kPadL;
-  return cuda_status(s2d5_advance(a, b, g0, nrows_global, bt, ring_hold, order, int(row_lo),
-                                  int(row_hi), static_cast<cudaStream_t>(stream)));
+  if (mirror_rows < 0 || mirror_rows > std::min<int64_t>(rows, kGhost))
+    return cuda_status(cudaErrorInvalidValue);
+  return cuda_status(s2d5_advance_p2p(a, b, g0, nrows_global, bt, ring_hold, order, int(row_lo),
+                                      int(row_hi), mirror_up, mirror_dn, int(mirror_rows),
+                                      static_cast<cudaStream_t>(stream)));
 }
 
 int pcotgpu_test_div9(const double* x, double* q_fast, double* q_ref, int64_t n, void* stream) {

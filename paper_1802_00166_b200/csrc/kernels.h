@@ -27,6 +27,13 @@ enum TileOrderMode { kOrderLex = 0, kOrderMorton = 1 };
 cudaError_t s2d5_advance(const Slab2D& in, const Slab2D& out, int64_t g0, int64_t nrows,
                          int bt, int ring_hold, int order, int row_lo, int row_hi,
                          cudaStream_t stream);
+// Same, and the owned rows [0, mirror_rows) / [rows - mirror_rows, rows) of the
+// output are also stored at mirror_up / mirror_dn + row * out.ld + col (peer
+// ghost rows, P2P over NVLink); a null mirror is skipped.
+cudaError_t s2d5_advance_p2p(const Slab2D& in, const Slab2D& out, int64_t g0, int64_t nrows,
+                             int bt, int ring_hold, int order, int row_lo, int row_hi,
+                             double* mirror_up, double* mirror_dn, int mirror_rows,
+                             cudaStream_t stream);
 int s2d5_max_bt();
 
 // 3-D 7-point, dense N^3 cube with halo padding (see Grid3D).

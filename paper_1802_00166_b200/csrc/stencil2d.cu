@@ -57,6 +57,13 @@ struct S2Args {
   int nstrips, nchunks;
   int order;
   int w_out;
+  // In-kernel halo exchange (row-sharded grids, P2P over NVLink): output rows
+  // [row_lo, mir_lo) are also stored at mir_up + row*ld_out + col (the upper
+  // neighbour's ghost rows below its slab), rows [mir_hi, row_hi) at mir_dn
+  // + row*ld_out + col (the lower neighbour's ghost rows); null = no mirror.
+  double* mir_up;
+  double* mir_dn;
+  int64_t mir_lo, mir_hi;
 };
 
 // Tile id -> (strip, chunk): lexicographic (SLT-like) or Morton/Z order over a
@@ -200,7 +207,8 @@ PCOT_DEV void s2d5_iter(Regs<BT, C>& R, const double* __restrict__ ring_row, uin
       // smask: this thread's output columns.  Halo threads (mask 0) skip the
       // store without a divergent scalar path; only grid-edge strips have
       // partially covered threads.
-      double* dst = a.out + int64_t(rho) * a.ld_out + cb;
+      const int64_t off = int64_t(rho) * a.ld_out + cb;
+      double* dst = a.out + off;
       if (SHIFT == 0 && C % 2 == 0 && smask == (1u << C) - 1u) {
 #pragma unroll
         for (int c = 0; c < C; c += 2)
@@ -212,6 +220,25 @@ PCOT_DEV void s2d5_iter(Regs<BT, C>& R, const double* __restrict__ ring_row, uin
 #pragma unroll
         for (int c = 0; c < C; ++c)
           if ((smask >> c) & 1u) __stcs(dst + c, nv[c]);
+      }
+      // P2P halo: the same values into the neighbour's ghost row.  Compiled
+      // only into the row-edge body (MASK bit 2), which the tiles holding a
+      // shard's first/last bt rows run for those rows; the interior body —
+      // nearly all of the work — carries no extra code or registers.
+      double* md = nullptr;
+      if constexpr ((MASK & 2) != 0)
+        md = rho < a.mir_lo ? a.mir_up : (rho >= a.mir_hi ? a.mir_dn : nullptr);
+      if (md != nullptr) {
+        md += off;
+        if (SHIFT == 0 && C % 2 == 0 && smask == (1u << C) - 1u) {
+#pragma unroll
+          for (int c = 0; c < C; c += 2)
+            *reinterpret_cast<double2*>(md + c) = make_double2(nv[c], nv[c + 1]);
+        } else if (smask != 0u && smask != (1u << C) - 1u) {
+#pragma unroll
+          for (int c = 0; c < C; ++c)
+            if ((smask >> c) & 1u) md[c] = nv[c];
+        }
       }
     }
   }
@@ -279,7 +306,11 @@ PCOT_DEV void s2d5_tile(const S2Args& a, int strip, int chunk, double* ring, uin
   // Row-edge chunks need the row mask only while some level's row is on or
   // outside the ring: input rows k with every level's row k-1-L (L < BT) in
   // [1, nrows-2] (global) run the unmasked body.
-  const int64_t k_safe_lo = 1 - a.g0 + BT, k_safe_hi = a.nrows - 1 - a.g0;
+  // The same holds for the rows whose last level is mirrored to a neighbour
+  // (rho = k - BT in [0, mir_lo) or [mir_hi, rows)).
+  int64_t k_safe_lo = 1 - a.g0 + BT, k_safe_hi = a.nrows - 1 - a.g0;
+  if (a.mir_up != nullptr && a.mir_lo + BT > k_safe_lo) k_safe_lo = a.mir_lo + BT;
+  if (a.mir_dn != nullptr && a.mir_hi - 1 + BT < k_safe_hi) k_safe_hi = a.mir_hi - 1 + BT;
   // The TMA refill rotates over the warps (lane 0): the ~30 issue
   // instructions would otherwise make warp 0 the last to reach every barrier.
   constexpr int NW = NT / 32;
@@ -340,7 +371,9 @@ __global__ void __launch_bounds__(NT, MINB) s2d5_kernel(S2Args a) {
   // Tiles whose dependence cone touches the ring (or the outside) need masks:
   // column-edge strips per element, row-edge chunks by a uniform row test.
   const bool edge_c = (c0 - BT <= 0) || (c0 + a.w_out + BT >= a.cols - 1);
-  const bool edge_r = (a.g0 + r0 - BT <= 0) || (a.g0 + r1 + BT >= a.nrows - 1);
+  const bool edge_r = (a.g0 + r0 - BT <= 0) || (a.g0 + r1 + BT >= a.nrows - 1) ||
+                      (a.mir_up != nullptr && r0 < a.mir_lo) ||
+                      (a.mir_dn != nullptr && r1 > a.mir_hi);
   const int mk = (edge_c ? 1 : 0) | (edge_r ? 2 : 0);
   if (mk == 0)
     s2d5_tile<BT, C, NT, 0, HOLD, XS, kPF>(a, strip, chunk, ring, bars, edge);
@@ -488,6 +521,15 @@ int s2d5_window_cols() { return 1024 + 2; }
 cudaError_t s2d5_advance(const Slab2D& in, const Slab2D& out, int64_t g0, int64_t nrows,
                          int bt, int ring_hold, int order, int row_lo, int row_hi,
                          cudaStream_t stream) {
+  return s2d5_advance_p2p(in, out, g0, nrows, bt, ring_hold, order, row_lo, row_hi, nullptr,
+                          nullptr, 0, stream);
+}
+
+cudaError_t s2d5_advance_p2p(const Slab2D& in, const Slab2D& out, int64_t g0, int64_t nrows,
+                             int bt, int ring_hold, int order, int row_lo, int row_hi,
+                             double* mirror_up, double* mirror_dn, int mirror_rows,
+                             cudaStream_t stream) {
+  if (mirror_rows < 0 || mirror_rows > out.rows) return cudaErrorInvalidValue;
   if (bt < 1 || bt > 8) return cudaErrorInvalidValue;
   if (row_hi <= row_lo) return cudaSuccess;
   if (in.ghost < bt + 3 || in.padl < bt + 1) return cudaErrorInvalidValue;
@@ -505,6 +547,10 @@ cudaError_t s2d5_advance(const Slab2D& in, const Slab2D& out, int64_t g0, int64_
   a.load_lo = -in.ghost;
   a.load_hi = in.rows + in.ghost - 1;
   a.order = order;
+  a.mir_up = mirror_rows > 0 ? mirror_up : nullptr;
+  a.mir_dn = mirror_rows > 0 ? mirror_dn : nullptr;
+  a.mir_lo = mirror_rows;
+  a.mir_hi = out.rows - mirror_rows;
   static int variant = -2;
   if (variant == -2) {
     const char* v = std::getenv("PCOTGPU_S2D5_VARIANT");

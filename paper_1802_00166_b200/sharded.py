@@ -16,6 +16,14 @@ long as the ghost rows hold the neighbour's step-t0 values.
 
 The slab kernel is injected (`advance`) so the same exchange logic runs with
 the sm_100a kernel on GPUs and is tested with gloo on CPU.
+
+halo="p2p" fuses the exchange into the stencil kernel instead: both slabs
+live in symmetric memory (torch.distributed._symmetric_memory, peer buffers
+mapped over NVLink), one launch per block advances every owned row and
+stores its first/last bt output rows a second time, straight into the
+neighbours' ghost rows (`pcotgpu_s2d5_advance_p2p`); a device-side barrier on
+the stream then orders the block against the neighbours' next one.  No
+send/recv, no separate edge launches.
 """
 import ctypes
 
@@ -23,6 +31,16 @@ import torch
 import torch.distributed as dist
 
 import paper_1802_00166_b200 as P
+
+
+def mirror_targets(peer_out_origin_up, peer_out_origin_dn, rows, ld):
+    """Byte addresses the P2P kernel takes as mirror_up / mirror_dn: output row r
+    of this slab lands at mirror + (r*ld + col)*8, i.e. the upper neighbour's
+    row R + r (its ghost rows below, r < bt) and the lower neighbour's row r - R
+    (its ghost rows above, r >= R - bt).  None = no neighbour on that side."""
+    up = None if peer_out_origin_up is None else peer_out_origin_up + rows * ld * 8
+    dn = None if peer_out_origin_dn is None else peer_out_origin_dn - rows * ld * 8
+    return up, dn
 
 
 def layout(rows, cols):
@@ -37,7 +55,7 @@ class ShardedStencil2D:
     global grid's edges (ring_hold=0: literal 0.0, 1: copied forward)."""
 
     def __init__(self, rows_per_rank, cols, T, bt, ring_hold=0, order=0, device=None,
-                 advance=None, geometry=None, group=None):
+                 advance=None, geometry=None, group=None, halo="nccl"):
         self.rank = dist.get_rank() if dist.is_initialized() else 0
         self.world = dist.get_world_size() if dist.is_initialized() else 1
         self.group = group
@@ -53,10 +71,26 @@ class ShardedStencil2D:
         self.ld, self.ghost, self.padl, total = geometry
         if self.ghost < self.bt + 3:
             raise ValueError("ghost rows < bt + 3")
-        self.buf = [torch.zeros(total, dtype=torch.float64, device=self.device) for _ in range(2)]
+        self.on_gpu = self.device.type == "cuda"
+        if halo not in ("nccl", "p2p"):
+            raise ValueError("halo must be 'nccl' or 'p2p'")
+        self.p2p = halo == "p2p" and self.world > 1
+        if self.p2p and not self.on_gpu:
+            raise ValueError("halo='p2p' needs CUDA devices (peer memory over NVLink)")
+        if self.p2p:
+            from torch.distributed import _symmetric_memory as symm
+
+            grp = self.group if self.group is not None else dist.group.WORLD
+            self.buf, self.symm = [], []
+            for _ in range(2):
+                t = symm.empty(total, dtype=torch.float64, device=self.device)
+                t.zero_()
+                self.buf.append(t)
+                self.symm.append(symm.rendezvous(t, grp))
+        else:
+            self.buf = [torch.zeros(total, dtype=torch.float64, device=self.device) for _ in range(2)]
         self.cur = 0
         self.advance = advance or self._advance_cuda
-        self.on_gpu = self.device.type == "cuda"
         if self.on_gpu:
             self.s_edge = torch.cuda.Stream(device=self.device, priority=-1)
             self.s_inner = torch.cuda.Stream(device=self.device)
@@ -137,6 +171,19 @@ class ShardedStencil2D:
             self.g0, self.nrows, bt, self.ring_hold, self.order, row_lo, row_hi,
             ctypes.c_void_p(stream.cuda_stream if stream is not None else 0)))
 
+    def _peer_origin(self, b, peer):
+        if peer < 0 or peer >= self.world:
+            return None
+        return int(self.symm[b].buffer_ptrs[peer]) + self.origin_offset() * 8
+
+    def _advance_p2p(self, src, dst, bt, stream):
+        up, dn = mirror_targets(self._peer_origin(dst, self.rank - 1),
+                                self._peer_origin(dst, self.rank + 1), self.R, self.ld)
+        P._check(P.lib().pcotgpu_s2d5_advance_p2p(
+            ctypes.c_void_p(self.ptr(src)), ctypes.c_void_p(self.ptr(dst)), self.R, self.cols,
+            self.g0, self.nrows, bt, self.ring_hold, self.order, 0, self.R,
+            ctypes.c_void_p(up), ctypes.c_void_p(dn), bt, ctypes.c_void_p(stream.cuda_stream)))
+
     def _timed(self, fn, stream, record):
         if record and self.on_gpu:
             e0 = torch.cuda.Event(enable_timing=True)
@@ -157,6 +204,14 @@ class ShardedStencil2D:
         elif not self.on_gpu:
             self.advance(src, dst, 0, self.R, bt, None)
             self.exchange_sync(dst, bt)
+        elif self.p2p:
+            # one launch: owned rows + their mirror stores into the neighbours'
+            # ghost rows of `dst`; the barrier (after this kernel, on the same
+            # stream) waits for the neighbours' kernels of this block, whose
+            # stores filled our ghost rows, before anyone starts the next block
+            main = torch.cuda.current_stream(self.device)
+            self._timed(lambda: self._advance_p2p(src, dst, bt, main), main, record)
+            self.symm[dst].barrier(channel=0)
         else:
             main = torch.cuda.current_stream(self.device)
             self.s_edge.wait_stream(main)
@@ -187,4 +242,4 @@ class ShardedStencil2D:
 
     def launches_per_run(self):
         blocks = -(-self.T // self.bt)
-        return blocks * (1 if self.world == 1 else 3)
+        return blocks * (1 if self.world == 1 or self.p2p else 3)

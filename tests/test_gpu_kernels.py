@@ -148,3 +148,49 @@ def test_launch_modes_bit_exact(env):
     p = subprocess.run([sys.executable, "-c", code], cwd=O.REPO, env=e, capture_output=True,
                        text=True, timeout=900)
     assert p.returncode == 0 and "ok" in p.stdout, p.stdout + p.stderr
+
+
+def test_p2p_halo_mirror_stores_equal_single_grid():
+    """The fused halo exchange of `ShardedStencil2D(halo="p2p")` on one GPU: two
+    row shards in one process, each launch also storing its first/last bt
+    output rows into the other shard's ghost rows (`pcotgpu_s2d5_advance_p2p`,
+    addresses from `sharded.mirror_targets`), launches stream-ordered (no
+    kernel waits on another).  No ghost row is copied after the start, so the
+    result equals the single grid only if every mirror store lands in place."""
+    import ctypes
+
+    import torch
+
+    from paper_1802_00166_b200.sharded import layout, mirror_targets
+
+    N, T, bt = 600, 20, 6
+    R = N // 2
+    ld, ghost, padl, total = layout(R, N)
+    dev = torch.device("cuda", 0)
+    s = torch.cuda.current_stream(dev)
+    lib = P.lib()
+    buf = [[torch.zeros(total, dtype=torch.float64, device=dev) for _ in range(2)] for _ in range(2)]
+    org = lambda k, b: buf[k][b].data_ptr() + (ghost * ld + padl) * 8  # noqa: E731
+    for k in range(2):
+        P._check(lib.pcotgpu_fill_init_value(ctypes.c_void_p(org(k, 0)), ld, R, N, b"F", k * R * N,
+                                             ctypes.c_void_p(s.cuda_stream)))
+        P._check(lib.pcotgpu_s2d5_prepare(ctypes.c_void_p(org(k, 0)), R, N, k * R, N, 0,
+                                          ctypes.c_void_p(s.cuda_stream)))
+    rows = lambda k, b, r0, r1: buf[k][b][(ghost + r0) * ld:(ghost + r1) * ld]  # noqa: E731
+    rows(0, 0, R, R + ghost).copy_(rows(1, 0, 0, ghost))   # initial ghosts only
+    rows(1, 0, -ghost, 0).copy_(rows(0, 0, R - ghost, R))
+    cur, t = 0, 0
+    while t < T:
+        step = min(bt, T - t)
+        for k in range(2):
+            up, dn = mirror_targets(org(0, cur ^ 1) if k == 1 else None,
+                                    org(1, cur ^ 1) if k == 0 else None, R, ld)
+            P._check(lib.pcotgpu_s2d5_advance_p2p(
+                ctypes.c_void_p(org(k, cur)), ctypes.c_void_p(org(k, cur ^ 1)), R, N, k * R, N, step,
+                0, 0, 0, R, ctypes.c_void_p(up), ctypes.c_void_p(dn), step,
+                ctypes.c_void_p(s.cuda_stream)))
+        cur ^= 1
+        t += step
+    got = torch.cat([rows(k, cur, 0, R).view(R, ld)[:, padl:padl + N] for k in range(2)]).cpu().numpy()
+    want = O.reference_output("jacobi2d", {"T": T, "N": N}).reshape(N, N)
+    assert np.array_equal(got.view(np.uint64), want.view(np.uint64))

@@ -80,3 +80,26 @@ def test_two_rank_halo_exchange_matches_single_grid(N, T, bt):
         assert p.exitcode == 0
     want = O.reference_output("jacobi2d", {"T": T, "N": N}).reshape(N, N)
     assert np.array_equal(got.view(np.uint64), want.view(np.uint64))
+
+
+def test_p2p_mirror_targets_address_neighbour_ghost_rows():
+    """halo="p2p": output row r of rank k, stored at mirror + (r*ld + c)*8, must be
+    the upper neighbour's row R + r (r < bt) and the lower neighbour's row r - R
+    (r >= R - bt) — the rows the NCCL path sends (`_ops`)."""
+    from paper_1802_00166_b200.sharded import mirror_targets
+
+    R, ld, bt = 40, 96, 5
+    up_origin, dn_origin = 1 << 30, 1 << 34
+    up, dn = mirror_targets(up_origin, dn_origin, R, ld)
+    for r in range(bt):
+        assert up + (r * ld + 7) * 8 == up_origin + ((R + r) * ld + 7) * 8
+    for r in range(R - bt, R):
+        assert dn + (r * ld + 7) * 8 == dn_origin + ((r - R) * ld + 7) * 8
+    assert mirror_targets(None, None, R, ld) == (None, None)
+
+
+def test_halo_mode_is_validated():
+    from paper_1802_00166_b200.sharded import ShardedStencil2D
+
+    with pytest.raises(ValueError):
+        ShardedStencil2D(16, 16, 4, 2, halo="udp", geometry=(16, 8, 2, 16 * 32))
