@@ -232,7 +232,9 @@ def main():
 
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if world > 1:
+    if world > 1 or args.halo == "p2p":
+        if "MASTER_ADDR" not in os.environ:  # --halo p2p on one GPU without torchrun
+            os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT="29541", RANK="0", WORLD_SIZE="1")
         dist.init_process_group("nccl", device_id=dev)
     rows = args.rows if args.scaling == "weak" else args.rows // world
     S = ShardedStencil2D(rows, args.cols, args.T, args.bt, ring_hold=0,
@@ -348,7 +350,7 @@ def main():
             "fp64_updates_per_step": updates,
         }
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if dist.is_initialized():
         dist.destroy_process_group()
     return 0
 

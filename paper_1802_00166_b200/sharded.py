@@ -74,9 +74,11 @@ class ShardedStencil2D:
         self.on_gpu = self.device.type == "cuda"
         if halo not in ("nccl", "p2p"):
             raise ValueError("halo must be 'nccl' or 'p2p'")
-        self.p2p = halo == "p2p" and self.world > 1
-        if self.p2p and not self.on_gpu:
-            raise ValueError("halo='p2p' needs CUDA devices (peer memory over NVLink)")
+        # (at world size 1 the symmetric-memory path still runs: no neighbours,
+        # so no mirror stores, but the allocation, rendezvous and barrier do)
+        self.p2p = halo == "p2p"
+        if self.p2p and not (self.on_gpu and dist.is_initialized()):
+            raise ValueError("halo='p2p' needs CUDA devices and an initialised process group")
         if self.p2p:
             from torch.distributed import _symmetric_memory as symm
 
@@ -198,7 +200,7 @@ class ShardedStencil2D:
     def block(self, bt, record=False):
         """Advance all owned rows by bt steps, exchanging boundary rows."""
         src, dst = self.cur, self.cur ^ 1
-        if self.world == 1:
+        if self.world == 1 and not self.p2p:
             stream = torch.cuda.current_stream(self.device) if self.on_gpu else None
             self._timed(lambda: self.advance(src, dst, 0, self.R, bt, stream), stream, record)
         elif not self.on_gpu:

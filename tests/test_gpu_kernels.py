@@ -194,3 +194,31 @@ def test_p2p_halo_mirror_stores_equal_single_grid():
     got = torch.cat([rows(k, cur, 0, R).view(R, ld)[:, padl:padl + N] for k in range(2)]).cpu().numpy()
     want = O.reference_output("jacobi2d", {"T": T, "N": N}).reshape(N, N)
     assert np.array_equal(got.view(np.uint64), want.view(np.uint64))
+
+
+def test_sharded_p2p_mode_runs_through_symmetric_memory():
+    """`ShardedStencil2D(halo="p2p")` at world size 1 (NCCL group of one): the
+    symmetric-memory allocation, rendezvous, kernel launches with (null)
+    mirrors and the per-block device barrier all run; result = oracle."""
+    import subprocess
+    import sys
+
+    code = (
+        "import os, numpy as np, torch, torch.distributed as dist\n"
+        "os.environ.update(MASTER_ADDR='127.0.0.1', MASTER_PORT='29547', RANK='0', WORLD_SIZE='1')\n"
+        "dev = torch.device('cuda', 0); torch.cuda.set_device(dev)\n"
+        "dist.init_process_group('nccl', device_id=dev)\n"
+        "from paper_1802_00166_b200.sharded import ShardedStencil2D\n"
+        "from tests import oracle_ctypes as O\n"
+        "N, T = 515, 23\n"
+        "S = ShardedStencil2D(N, N, T, 6, device=dev, halo='p2p')\n"
+        "assert S.p2p and len(S.symm) == 2\n"
+        "S.fill_init('F'); S.run(); torch.cuda.synchronize()\n"
+        "got = S.interior(S.cur).cpu().numpy()\n"
+        "want = O.reference_output('jacobi2d', {'T': T, 'N': N}).reshape(N, N)\n"
+        "assert np.array_equal(got.view(np.uint64), want.view(np.uint64))\n"
+        "dist.destroy_process_group()\n"
+        "print('ok')\n")
+    p = subprocess.run([sys.executable, "-c", code], cwd=O.REPO, capture_output=True, text=True,
+                       timeout=600)
+    assert p.returncode == 0 and "ok" in p.stdout, p.stdout + p.stderr
