@@ -35,6 +35,8 @@ cudaError_t s2d5_advance_p2p(const Slab2D& in, const Slab2D& out, int64_t g0, in
                              double* mirror_up, double* mirror_dn, int mirror_rows,
                              cudaStream_t stream);
 int s2d5_max_bt();
+// Programmatic dependent launch for the stencil depth blocks (PCOTGPU_PDL=0: off).
+bool pdl_enabled();
 
 // 3-D 7-point, dense N^3 cube with halo padding (see Grid3D).
 struct Grid3D {

@@ -28,8 +28,6 @@
 
 namespace pcotgpu {
 
-bool pdl_enabled();  // stencil2d.cu
-
 namespace {
 
 // PCOTGPU_S3D7_CHUNKS: tuning override of the plane chunking (tools/kbench.py s3d7)
