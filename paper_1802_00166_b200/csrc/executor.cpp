@@ -185,7 +185,7 @@ struct GpuExecutor::Impl {
         const int64_t ld = round_up(kPadL + n + kPadR2, 16);
         for (int b = 0; b < 2; ++b) {
           slab[b].alloc(size_t((n + 2 * kGhost) * ld));
-          ck(cudaMemset(slab[b].p, 0, slab[b].n * sizeof(double)), "cudaMemset");
+          ck(cudaMemsetAsync(slab[b].p, 0, slab[b].n * sizeof(double), stream), "cudaMemset");
           sg[b].origin = slab[b].p + kGhost * ld + kPadL;
           sg[b].ld = ld;
           sg[b].rows = n;
@@ -201,7 +201,7 @@ struct GpuExecutor::Impl {
         const int64_t pi = pj * (n + 2 * kGhost);
         for (int b = 0; b < 2; ++b) {
           cube[b].alloc(size_t(pi * (n + 2 * kGhost)));
-          ck(cudaMemset(cube[b].p, 0, cube[b].n * sizeof(double)), "cudaMemset");
+          ck(cudaMemsetAsync(cube[b].p, 0, cube[b].n * sizeof(double), stream), "cudaMemset");
           cg[b].origin = cube[b].p + kGhost * pi + kGhost * pj + kGhost;
           cg[b].n = n;
           cg[b].pitch_j = pj;
@@ -222,7 +222,9 @@ struct GpuExecutor::Impl {
         in_ld = g_ld;
         for (int q = 0; q < 2; ++q) {
           in[q].alloc(size_t(n * g_ld));
-          ck(cudaMemset(in[q].p, 0, in[q].n * sizeof(double)), "cudaMemset");
+          // on the executor's stream: a legacy-stream cudaMemset is not ordered
+          // with the non-blocking stream's init kernels and raced them
+          ck(cudaMemsetAsync(in[q].p, 0, in[q].n * sizeof(double), stream), "cudaMemset");
         }
         gA.alloc(size_t(n * g_ld));
         gB.alloc(size_t(n * g_ld));

@@ -326,6 +326,9 @@ T* upload(const std::vector<T>& v) {
   if (v.empty()) return nullptr;
   ckc(cudaMalloc(&d, v.size() * sizeof(T)), "cudaMalloc");
   ckc(cudaMemcpy(d, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice), "H2D");
+  // pageable H2D on the legacy stream may still be in flight on return, and the
+  // executor's non-blocking stream does not wait for the legacy stream
+  ckc(cudaStreamSynchronize(0), "H2D");
   return d;
 }
 

@@ -818,6 +818,7 @@ GsPlan* gs2d_plan_create(int64_t n, int64_t T, int bt, int bx, int by, int devic
   cudaMalloc(&p->d_state, (p->ntiles + 1) * sizeof(int));
   cudaMemcpy(p->d_tiles, tiles.data(), tiles.size() * sizeof(int), cudaMemcpyHostToDevice);
   cudaMemcpy(p->d_preds, preds.data(), preds.size() * sizeof(int), cudaMemcpyHostToDevice);
+  cudaStreamSynchronize(0);  // legacy-stream copies vs the caller's non-blocking stream
   const int ni = bx + bt + 1, ns = by + 2 * bt + 2;
   const int kind = gs_kind(bt, bx);
   const size_t smem = size_t(ni) * ns * (kind ? 9 : 8) + 16;
