@@ -16,7 +16,15 @@ Metric: stencil GUpdates/s (whole job), plus
               (pcotgpu_run_batch: the copies of adjacent steps overlap compute);
   cpu_baseline — the reference's own tiled CPU path (its emitted C, OpenMP,
               all host cores) on a bounded sample, rank 0, N=1.
+  per_config — BASELINE configs 0-3 in the same run (N=1, rank 0): each
+              through the executor's default schedule, CUDA-event timed with
+              an L2 flush before every timed run, clocks sampled, output
+              checksum against the reference golden (config 3: 4096 sampled
+              cells of the reference's result, componentwise 1e-12), roofline
+              fraction, and the reference's CPU path on a bounded sample.
 --impl reference runs only that reference CPU path (rank 0) on the sample.
+--gpus N without torchrun re-launches itself under torch.distributed.run with
+N ranks (NCCL_DEBUG=INFO); --dry-run checks the rank plumbing on CPU (gloo).
 """
 import argparse
 import json
@@ -124,20 +132,26 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sms)}
 
 
-def run_reference_sample(threads):
-    """Wall time of the reference's emitted C on the sample minus its init-only twin."""
+def run_reference_sample(threads, sample=SAMPLE, init=SAMPLE_INIT, leaf=None):
+    """Wall time of the reference's emitted C on a sample minus its init-only
+    twin; `leaf` overrides the binary's default leaf sizes (argv b0..)."""
     env = dict(os.environ)
     env["OMP_NUM_THREADS"] = str(threads)
 
-    def wall(tag):
+    def wall(tag, argv):
         b = os.path.join(EMIT_DIR, tag)
         t0 = time.perf_counter()
-        out = subprocess.run([b], capture_output=True, text=True, env=env, check=True)
+        out = subprocess.run([b] + argv, capture_output=True, text=True, env=env, check=True)
         return time.perf_counter() - t0, out.stdout.split()[1]
 
-    t_init, _ = wall(SAMPLE_INIT)
-    t_run, chk = wall(SAMPLE)
+    t_init, _ = wall(init, [])
+    t_run, chk = wall(sample, [str(x) for x in leaf] if leaf else [])
     return max(t_run - t_init, 1e-9), chk
+
+
+# leaf sizes (t, rows, cols) tried for the OpenMP sample; the best is the baseline
+LEAF_SWEEP = [(16, 128, 1024), (32, 128, 512), (8, 256, 2048)]
+SEQ_SAMPLE, SEQ_INIT, SEQ_UPDATES = "jacobi2d_N4096_T32_seq", "jacobi2d_N4096_T0_seq", 4096 * 4096 * 32
 
 
 def cpu_baseline_port(threads):
@@ -156,10 +170,37 @@ def reference_available():
         os.path.join(EMIT_DIR, SAMPLE_INIT))
 
 
+def host_info():
+    info = {"nproc": os.cpu_count()}
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    info["cpu_model"] = line.split(":", 1)[1].strip()
+                    break
+        with open("/proc/meminfo") as f:
+            info["mem_total_gib"] = round(int(f.readline().split()[1]) / 2**20, 1)
+    except OSError:
+        pass
+    return info
+
+
 def cpu_baseline(threads):
+    """Best of a leaf sweep of the reference's OpenMP path on the sample, plus
+    its sequential emitted C on a smaller sample (same rule)."""
+    sweep, seq = [], None
     if reference_available():
-        secs, chk = run_reference_sample(threads)
-        kind = "reference"
+        for leaf in LEAF_SWEEP:
+            secs, chk = run_reference_sample(threads, leaf=leaf)
+            sweep.append({"leaf": list(leaf), "seconds": round(secs, 3), "checksum": chk,
+                          "GUpdates/s": round(SAMPLE_UPDATES / secs / 1e9, 4)})
+        best = min(sweep, key=lambda e: e["seconds"])
+        secs, chk, kind = best["seconds"], best["checksum"], "reference"
+        if os.path.exists(os.path.join(EMIT_DIR, SEQ_SAMPLE)):
+            ssecs, _ = run_reference_sample(1, SEQ_SAMPLE, SEQ_INIT)
+            seq = {"value": SEQ_UPDATES / ssecs / 1e9, "unit": "GUpdates/s", "cores": 1,
+                   "seconds": round(ssecs, 3),
+                   "sample": "Jacobi-2D 4096^2, T=32, reference emitted C without OpenMP"}
     else:
         secs, chk = cpu_baseline_port(threads), None
         kind = "port"
@@ -167,7 +208,8 @@ def cpu_baseline(threads):
             "kind": kind, "seconds": round(secs, 3), "checksum": chk,
             "sample": "Jacobi-2D 8192^2, T=160 (same rule/ring/init as config 4; "
                       "reference emitted recursive C, OpenMP tasks, -O2 -ffp-contract=off; "
-                      "wall minus init-only run)"}
+                      "wall minus init-only run; best of the leaf sweep)",
+            "leaf_sweep": sweep, "sequential": seq, "host": host_info()}
 
 
 def reference_arm(args, rank, world):
@@ -176,13 +218,22 @@ def reference_arm(args, rank, world):
     threads = os.cpu_count() or 1
     times = []
     kind = "reference" if reference_available() else "port"
+    # warm-up steps walk the leaf sweep; the timed steps use the fastest leaf
+    warm = {}
     for i in range(args.warmup + args.steps):
         if kind == "reference":
-            secs, _ = run_reference_sample(threads)
+            if i < args.warmup:
+                leaf = LEAF_SWEEP[i % len(LEAF_SWEEP)]
+            else:
+                leaf = min(warm, key=warm.get) if warm else None
+            secs, _ = run_reference_sample(threads, leaf=leaf)
+            if i < args.warmup:
+                warm[leaf] = min(secs, warm.get(leaf, secs))
         else:
             secs = cpu_baseline_port(threads)
         if i >= args.warmup:
             times.append(secs)
+    best_leaf = list(min(warm, key=warm.get)) if warm else None
     ms = 1000.0 * sum(times) / len(times)
     value = SAMPLE_UPDATES / (ms / 1000.0) / 1e9
     line = {
@@ -191,13 +242,169 @@ def reference_arm(args, rank, world):
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (reference init_value)", "impl": "reference",
         "config": {"workload": "jacobi2d 8192x8192 T=160 (bounded CPU sample of config 4)",
-                   "parallelism": "OpenMP tasks, %d threads" % threads},
+                   "parallelism": "OpenMP tasks, %d threads" % threads, "leaf": best_leaf},
         "cpu_baseline": {"value": value, "unit": "GUpdates/s", "cores": threads, "kind": kind,
-                         "sample": "Jacobi-2D 8192^2 T=160, reference emitted C"},
+                         "sample": "Jacobi-2D 8192^2 T=160, reference emitted C, leaf %s "
+                                   "(fastest of the warm-up leaf sweep)" % best_leaf,
+                         "host": host_info()},
         "e2e": {"value": value, "unit": "GUpdates/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+    return 0
+
+
+# BASELINE configs 0-3, reported in the same driver run as config 4 (the headline):
+# (tag, kernel, params, reference CPU sample, its init-only twin, updates or flop of the sample)
+PER_CONFIG = [
+    ("cfg0", "jacobi2d", {"T": 256, "N": 2048}, "jacobi2d_N2048_T256", "jacobi2d_N2048_T0",
+     2048 * 2048 * 256),
+    ("cfg1", "heat3d_b", {"T": 100, "N": 384}, "heat3d_b_N384_T20", "heat3d_b_N384_T0", 384 ** 3 * 20),
+    ("cfg2", "gs2d", {"T": 64, "N": 4096}, "gs2d_N4096_T16", "gs2d_N4096_T0", 4096 * 4096 * 16),
+    ("cfg3", "gemm", {"N": 4096}, "gemm_N2048", "gemm_N1", 2 * 2048 ** 3),
+]
+
+
+def dmma_peak():
+    """Measured fp64 DMMA peak (tools/fp64_peaks.cu on this pool's B200)."""
+    try:
+        with open(os.path.join(REPO, "profiles", "fp64_peaks_r01.json")) as f:
+            d = json.load(f)
+        return max(r["TFLOPs"] for r in d["results"] if r["probe"].startswith("dmma")), "measured"
+    except (OSError, ValueError, KeyError):
+        return 40.0, "fallback (nominal B200 FP64 tensor)"
+
+
+def golden_checksum(kernel, params):
+    try:
+        with open(os.path.join(REPO, "tests", "golden", "golden.json")) as f:
+            for e in json.load(f)["entries"]:
+                if e["kernel"] == kernel and e["params"] == params:
+                    return e["checksum"]
+    except (OSError, ValueError):
+        pass
+    return None
+
+
+def gemm_sample_check(out, n):
+    """Config 3: componentwise error on the reference's 4096 sampled cells
+    (tests/golden/gemm4096_samples.json), bound 1e-12."""
+    import numpy as np
+
+    try:
+        with open(os.path.join(REPO, "tests", "golden", "gemm4096_samples.json")) as f:
+            g = json.load(f)
+    except (OSError, ValueError):
+        return {"status": "no sampled golden"}
+    if g["params"]["N"] != n:
+        return {"status": "sampled golden is for N=%d" % g["params"]["N"]}
+    rows = np.arange(n, dtype=np.int64)
+    cols = (rows * 2654435761 + 12345) % n
+    got = out.reshape(n, n)[rows, cols]
+    ref = np.array([int(h, 16) for h in g["out_hex"]], dtype=np.uint64).view(np.float64)
+    comp = float((np.abs(got - ref) / np.array(g["absab"])).max())
+    return {"cells": int(n), "componentwise_max": comp, "bound": 1e-12, "match": comp <= 1e-12,
+            "exact_cells": int((got.view(np.uint64) == ref.view(np.uint64)).sum())}
+
+
+def per_config(P, torch, dev, local, hbm_peak, reps_ms=1000.0):
+    """BASELINE configs 0-3 through the executor's default schedule (the path a
+    user of pcot::Executor gets), one GpuExecutor each."""
+    import numpy as np
+
+    flush = torch.empty(2 ** 30 // 8 * 2, dtype=torch.float64, device=dev)  # 2 GiB > L2 (126 MB)
+    dpeak, dpeak_src = dmma_peak()
+    res = []
+    threads = os.cpu_count() or 1
+    for tag, kernel, params, sample, init, sample_work in PER_CONFIG:
+        with P.GpuExecutor(kernel, params, device=local) as ex:
+            first = ex.run_untiled(skip_checksum=(kernel == "gemm"))
+            for _ in range(3):
+                ex.run_untiled(skip_checksum=True)
+            reps = int(max(5, min(200, reps_ms / max(first.device_ms, 1e-3))))
+            times = []
+            with ClockSampler(local) as clocks:
+                for _ in range(reps):
+                    flush.zero_()
+                    torch.cuda.synchronize(dev)
+                    times.append(ex.run_untiled(skip_checksum=True).device_ms)
+            ms = statistics.median(times)
+            e = {"config": tag, "kernel": kernel, "params": params, "bt": first.bt,
+                 "launches_per_run": int(first.launches), "timed_runs": reps,
+                 "ms_median": round(ms, 4), "ms_mean": round(statistics.mean(times), 4),
+                 "ms_cov": round(statistics.pstdev(times) / statistics.mean(times), 4),
+                 "l2": "2 GiB buffer written before every timed run"}
+            if kernel == "gemm":
+                n = params["N"]
+                tf = 2.0 * n ** 3 / (ms / 1e3) / 1e12
+                e["TFLOP/s"] = round(tf, 2)
+                e["roofline"] = {"bound": "fp64 tensor (DMMA)", "achieved": round(tf, 2), "peak": dpeak,
+                                 "unit": "TFLOP/s", "frac": round(tf / dpeak, 3), "peak_source": dpeak_src}
+                e["parity"] = gemm_sample_check(ex.array_data("Out"), n)
+            else:
+                nd = 3 if kernel.startswith("heat3d") else 2
+                upd = params["N"] ** nd * params["T"]
+                gu = upd / (ms / 1e3) / 1e9
+                e["GUpd/s"] = round(gu, 1)
+                if kernel == "gs2d":
+                    # in place: the grid crosses HBM once per launch of `seg` sweeps;
+                    # the bound is the update's dependence chain, not bytes
+                    fl = 11.0  # 8 DADD + div-by-9 (DMUL + 2 DFMA)
+                    dadd_peak = 18.4e12  # measured DADD issue (profiles/fp64_peaks_r01.json)
+                    e["roofline"] = {"bound": "fp64 dependence chain (in-place wavefront)",
+                                     "fp64_ops_per_update": fl,
+                                     "fp64_issue_frac": round(gu * 1e9 * fl / dadd_peak, 3),
+                                     "launches_per_run": int(first.launches)}
+                else:
+                    bpu = 16.0 / first.bt
+                    e["roofline"] = {"bound": "hbm", "bytes_per_update": bpu, "achieved": round(gu * bpu, 1),
+                                     "peak": hbm_peak, "unit": "GB/s", "frac": round(gu * bpu / hbm_peak, 3)}
+                want = golden_checksum(kernel, params)
+                e["parity"] = {"golden": want, "got": first.checksum_hex, "match": first.checksum_hex == want}
+            cl = clocks.summary()
+            e["clocks"] = {"sm_mhz": cl["sm_mhz"], "sm_max_mhz": cl["sm_max_mhz"], "reasons": cl["reasons"],
+                           "samples": cl["samples"]}
+        # the reference's own CPU path on a bounded sample of the same workload
+        if os.path.exists(os.path.join(EMIT_DIR, sample)):
+            secs, chk = run_reference_sample(threads, sample, init)
+            unit = "GFLOP/s" if kernel == "gemm" else "GUpdates/s"
+            e["cpu_baseline"] = {"value": round(sample_work / secs / 1e9, 4), "unit": unit, "cores": threads,
+                                 "kind": "reference", "seconds": round(secs, 3), "checksum": chk,
+                                 "sample": sample + " (reference emitted C, OpenMP, wall minus init-only run)"}
+        res.append(e)
+    del flush
+    return res
+
+
+def spawn_ranks(args):
+    """`--gpus N` outside torchrun: re-launch under torch.distributed.run with
+    one rank per GPU (the driver's own launch sets WORLD_SIZE and skips this)."""
+    import socket
+
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node",
+           str(args.gpus), "--master-addr", "127.0.0.1", "--master-port", str(port),
+           os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd, env=env)
+
+
+def dry_run(args, rank, world):
+    """Rank plumbing on CPU (gloo): every rank reports in, rank 0 prints the count."""
+    import torch
+    import torch.distributed as dist
+
+    dist.init_process_group("gloo")
+    t = torch.ones(1)
+    dist.all_reduce(t)
+    if rank == 0:
+        print(json.dumps({"dry_run": True, "n_gpus": world, "ranks_reporting": int(t.item()),
+                          "backend": "gloo"}), flush=True)
+    dist.destroy_process_group()
     return 0
 
 
@@ -218,11 +425,23 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-depth-sweep", action="store_true")
+    ap.add_argument("--no-per-config", action="store_true")
+    ap.add_argument("--dry-run", action="store_true", help="rank plumbing only (CPU, gloo)")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ and args.impl == "ours":
+        return spawn_ranks(args)
     rank, world, local = env_rank()
+    if args.impl == "ours" and "WORLD_SIZE" in os.environ and world != args.gpus:
+        sys.stderr.write("bench.py: --gpus %d but WORLD_SIZE=%d\n" % (args.gpus, world))
+        return 2
+    if args.dry_run:
+        return dry_run(args, rank, world)
 
     if args.impl == "reference":
         return reference_arm(args, rank, world)
+    if world > 1:
+        os.environ.setdefault("NCCL_DEBUG", "INFO")  # communicator lines for the driver's rank check
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
 
     import torch
     import torch.distributed as dist
@@ -330,6 +549,12 @@ def main():
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(os.cpu_count() or 1)
 
+    configs = None
+    if world == 1 and not args.no_per_config:
+        del S  # release config 4's slabs before the other configs allocate
+        torch.cuda.empty_cache()
+        configs = per_config(P, torch, dev, local, peak)
+
     if rank == 0:
         cl = clocks.summary()
         line = {
@@ -348,6 +573,7 @@ def main():
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
             "clocks": {"sm_mhz": cl["sm_mhz"], "sm_max_mhz": cl["sm_max_mhz"], "reasons": cl["reasons"]},
             "fp64_updates_per_step": updates,
+            "per_config": configs,
         }
         print(json.dumps(line), flush=True)
     if dist.is_initialized():

@@ -176,13 +176,9 @@ __global__ void affine_kernel(const double* __restrict__ x, double* __restrict__
 template <class G>
 cudaError_t launch_gemm(const double* A, const double* B, double* C, int64_t n, int64_t ld,
                         int order, int tiles_m, int tiles_n, int grid, cudaStream_t stream) {
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(dgemm_kernel<G>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, int(G::SMEM));
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
+  int sl = 0;
+  if (cudaError_t e = kernel_slots(reinterpret_cast<const void*>(dgemm_kernel<G>), G::NTHR, G::SMEM, &sl))
+    return e;
   dgemm_kernel<G><<<grid, G::NTHR, G::SMEM, stream>>>(A, B, C, int(n), ld, order, tiles_m, tiles_n);
   count_launch();
   return cudaGetLastError();
@@ -201,11 +197,7 @@ cudaError_t dgemm_nn(const double* A, const double* B, double* C, int64_t n, int
     while (side < tiles_m || side < tiles_n) side <<= 1;
     grid = side * side;
   }
-  static int variant = -2;
-  if (variant == -2) {
-    const char* v = std::getenv("PCOTGPU_DGEMM_VARIANT");
-    variant = v ? std::atoi(v) : 0;  // 0: default
-  }
+  const int variant = env_int("PCOTGPU_DGEMM_VARIANT", 0);  // 0: default
   // measured on the B200 at N=4096 (tools/kbench.py gemm; profiles/dgemm_r01.md)
   switch (variant) {
     case 1: return launch_gemm<GemmCfg<2, 4, 16, 4>>(A, B, C, n, ld, order, tiles_m, tiles_n, grid, stream);  // 28.2 TF/s

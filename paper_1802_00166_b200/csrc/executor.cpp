@@ -37,11 +37,6 @@ void ck(cudaError_t e, const char* what) {
 
 int64_t round_up(int64_t v, int64_t m) { return (v + m - 1) / m * m; }
 
-int env_int(const char* name, int dflt) {
-  const char* v = std::getenv(name);
-  return v ? std::atoi(v) : dflt;
-}
-
 constexpr int64_t kGhost = 16;  // ghost rows / halo planes (>= max bt + 3)
 constexpr int64_t kPadL = 16;   // left pad columns (128 B)
 constexpr int64_t kPadR2 = 1040; // right pad for the 2-D strip window (>= W_IN + 2, widest variant)
@@ -280,6 +275,14 @@ struct GpuExecutor::Impl {
     return bt;
   }
 
+  // A Gauss-Seidel dependence wait that timed out leaves an invalid grid:
+  // report it as a CUDA-level failure (PCOTGPU_E_CUDA), never a silent result.
+  void check_gs_fault() {
+    if (rec.family == Family::GaussSeidel2D9 && gs_plan && gs2d_plan_fault(gs_plan))
+      ck(cudaErrorLaunchTimeout, "Gauss-Seidel: a dependence wait hit its spin cap "
+                                 "(CTAs not co-resident?); the grid is invalid");
+  }
+
   int run_gs(const TileOrder& o) {
     // default tile = best measured (profiles/kbench_r01.md)
     int bt = env_int("PCOTGPU_GS_BT", 2), bx = env_int("PCOTGPU_GS_BX", 64),
@@ -339,6 +342,7 @@ struct GpuExecutor::Impl {
     }
     ck(cudaEventRecord(ev1, stream), "cudaEventRecord");
     ck(cudaEventSynchronize(ev1), "run");
+    check_gs_fault();
     float ms = 0;
     ck(cudaEventElapsedTime(&ms, ev0, ev1), "cudaEventElapsedTime");
     r.device_ms = ms;
@@ -543,6 +547,7 @@ struct GpuExecutor::Impl {
     ck(cudaStreamWaitEvent(stream, e_free, 0), "wait");
     ck(cudaEventRecord(ev1, stream), "cudaEventRecord");
     ck(cudaEventSynchronize(ev1), "run_batch");
+    check_gs_fault();
     float ms = 0;
     ck(cudaEventElapsedTime(&ms, ev0, ev1), "cudaEventElapsedTime");
     r.device_ms = ms;

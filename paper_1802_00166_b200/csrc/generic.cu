@@ -50,6 +50,8 @@ struct GDev {
   double* const* arr;
   const int64_t* fbase;  // first flag of each array
   unsigned* flags;       // dataflow: 1 = cell holds its final value; count pass: writes
+  unsigned long long* writer;  // count pass: min over writes of (point * nstmt + statement)
+  unsigned* bad;               // order pass: 1 if a read precedes (or is) its cell's write
   unsigned long long* next;
   unsigned long long* cnt;  // points, reads, writes
   int* err;                 // 0 ok; s+1: out-of-extent in statement s; -1: wait cap
@@ -179,6 +181,34 @@ __global__ void generic_count_kernel(GDev g) {
         continue;
       }
       atomicAdd(g.flags + g.fbase[w.array] + f, 1u);
+      atomicMin(g.writer + g.fbase[w.array] + f, p * (unsigned long long)g.nstmt + si);
+    }
+  }
+}
+
+// The dataflow grid makes every read wait for its cell's (single) write.  That
+// reproduces the reference only if, in the reference's order, the write comes
+// strictly before the read: a read of a cell written later (or by the reading
+// statement itself, whose write follows its body) sees the old value there.
+// Flags such kernels so they run in the reference's sequential order instead.
+__global__ void generic_order_kernel(GDev g) {
+  int64_t z[kMaxIdx];
+  for (unsigned long long p = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x;
+       p < (unsigned long long)g.npoints; p += (unsigned long long)gridDim.x * blockDim.x) {
+    decode(g, p, z);
+    for (int si = 0; si < g.nstmt; ++si) {
+      const GStmt s = g.st[si];
+      if (!in_domain(g, s, z)) continue;
+      const unsigned long long me = p * (unsigned long long)g.nstmt + si;
+      for (int o = 0; o < s.nops; ++o) {
+        const GOp op = g.ops[s.op0 + o];
+        if (op.kind != ORead) continue;
+        const GRef& r = g.refs[op.arg];
+        int64_t f = 0;
+        if (!cell_of(g, r, z, &f)) continue;  // reported by the run itself
+        const unsigned long long w = g.writer[g.fbase[r.array] + f];
+        if (w != ~0ull && w >= me) atomicOr(g.bad, 1u);
+      }
     }
   }
 }
@@ -309,7 +339,8 @@ struct GenericPlan {
   unsigned* d_flags0 = nullptr;  // initial flags (dataflow)
   unsigned long long* d_misc = nullptr;  // next, points, reads, writes
   int* d_err = nullptr;
-  unsigned* d_maxc = nullptr;
+  unsigned* d_maxc = nullptr;  // [0] max writes per cell, [1] order violation
+  unsigned long long* d_writer = nullptr;
   bool dataflow = false;
   bool counted = false;
 };
@@ -513,7 +544,7 @@ GenericPlan* generic_plan_create(const KernelSpec& k, const IntVec& prm, int dev
   ckc(cudaMalloc(&P->d_flags0, std::max<int64_t>(P->nflags, 1) * sizeof(unsigned)), "cudaMalloc");
   ckc(cudaMalloc(&P->d_misc, 4 * sizeof(unsigned long long)), "cudaMalloc");
   ckc(cudaMalloc(&P->d_err, sizeof(int)), "cudaMalloc");
-  ckc(cudaMalloc(&P->d_maxc, sizeof(unsigned)), "cudaMalloc");
+  ckc(cudaMalloc(&P->d_maxc, 2 * sizeof(unsigned)), "cudaMalloc");
   return P.release();
 }
 
@@ -532,6 +563,7 @@ void generic_plan_destroy(GenericPlan* p) {
   cudaFree(p->d_misc);
   cudaFree(p->d_err);
   cudaFree(p->d_maxc);
+  cudaFree(p->d_writer);
   delete p;
 }
 
@@ -588,25 +620,34 @@ cudaError_t generic_run(GenericPlan* p, cudaStream_t s, GenericCounts* counts, s
   if (!p->counted) {  // write counts once per plan: single assignment -> dataflow grid
     if ((e = cudaMemsetAsync(p->d_flags, 0, std::max<int64_t>(p->nflags, 1) * sizeof(unsigned), s)) != cudaSuccess)
       return e;
-    if ((e = cudaMemsetAsync(p->d_maxc, 0, sizeof(unsigned), s)) != cudaSuccess) return e;
+    if ((e = cudaMemsetAsync(p->d_maxc, 0, 2 * sizeof(unsigned), s)) != cudaSuccess) return e;
+    const size_t wbytes = size_t(std::max<int64_t>(p->nflags, 1)) * sizeof(unsigned long long);
+    if ((e = cudaMalloc(&p->d_writer, wbytes)) != cudaSuccess) return e;
+    if ((e = cudaMemsetAsync(p->d_writer, 0xff, wbytes, s)) != cudaSuccess) return e;
+    g.writer = p->d_writer;
+    g.bad = p->d_maxc + 1;
     if (p->npoints > 0) {
       generic_count_kernel<<<sms * 8, 256, 0, s>>>(g);
+      count_launch();
+      generic_order_kernel<<<sms * 8, 256, 0, s>>>(g);
       count_launch();
     }
     if (p->nflags > 0) {
       generic_flags_kernel<<<sms * 4, 256, 0, s>>>(p->d_flags, p->nflags, p->d_maxc);
       count_launch();
     }
-    unsigned maxc = 0;
+    unsigned maxc[2] = {0, 0};
     int err = 0;
-    if ((e = cudaMemcpyAsync(&maxc, p->d_maxc, sizeof(unsigned), cudaMemcpyDeviceToHost, s)) != cudaSuccess) return e;
+    if ((e = cudaMemcpyAsync(maxc, p->d_maxc, 2 * sizeof(unsigned), cudaMemcpyDeviceToHost, s)) != cudaSuccess) return e;
     if ((e = cudaMemcpyAsync(&err, p->d_err, sizeof(int), cudaMemcpyDeviceToHost, s)) != cudaSuccess) return e;
     if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return e;
     if (err > 0) {
       if (err_msg) *err_msg = "out-of-extent write in statement " + p->stmt_ids[size_t(err - 1)];
       return cudaErrorInvalidValue;
     }
-    p->dataflow = maxc <= 1;
+    cudaFree(p->d_writer);  // only the counting pass needs it
+    p->d_writer = nullptr;
+    p->dataflow = maxc[0] <= 1 && maxc[1] == 0;
     if ((e = cudaMemcpyAsync(p->d_flags0, p->d_flags, std::max<int64_t>(p->nflags, 1) * sizeof(unsigned),
                              cudaMemcpyDeviceToDevice, s)) != cudaSuccess)
       return e;

@@ -45,6 +45,11 @@ struct GsPlan {
   int64_t ebld = 0, ld = 0;
   double* wb[2] = {nullptr, nullptr};
   double* eb = nullptr;
+  // fault word: a dependence wait that hit its spin cap (lost co-residency or
+  // a scheduling bug) sets it; gs2d_run copies it to h_err after its launches
+  int* d_err = nullptr;
+  int* h_err = nullptr;  // pinned
+  bool setup_failed = false;
 };
 
 namespace {
@@ -73,9 +78,15 @@ __global__ void div9_check_kernel(const double* x, double* q_fast, double* q_ref
 // Acquire-spin on a predecessor's completion flag with exponential backoff:
 // thousands of resident warps may be waiting on the wavefront at once, and
 // tight polling would flood L2 with acquire loads.
-PCOT_DEV void spin_flag(const int* f) {
+// Bounded (~tens of seconds): on timeout the fault word is set and the run
+// reports an error instead of hanging the device or returning silently.
+PCOT_DEV void spin_flag(const int* f, int* err) {
   unsigned ns = 64;
-  while (ld_acquire(f) == 0) {
+  for (long long it = 0; ld_acquire(f) == 0; ++it) {
+    if (it > 20000000LL) {
+      atomicOr(err, 1);
+      return;
+    }
     __nanosleep(ns);
     ns = ns < 2048 ? ns * 2 : 2048;
   }
@@ -91,6 +102,7 @@ struct GsArgs {
   const int* preds;
   int* flags;
   int* counter;
+  int* err;
 };
 
 __global__ void gs2d_kernel(GsArgs g) {
@@ -107,7 +119,7 @@ __global__ void gs2d_kernel(GsArgs g) {
     if (tid < 8) {
       const int p = g.preds[tile * 8 + tid];
       if (p >= 0)
-        spin_flag(g.flags + p);
+        spin_flag(g.flags + p, g.err);
     }
     __syncthreads();
     const int64_t t0 = 1 + int64_t(tb) * g.bt;
@@ -185,7 +197,7 @@ __global__ void __launch_bounds__(32) gs2d_warp_kernel(GsArgs g) {
     if (lane < 8) {
       const int p = g.preds[tile * 8 + lane];
       if (p >= 0)
-        spin_flag(g.flags + p);
+        spin_flag(g.flags + p, g.err);
     }
     __syncwarp();
     const int t0 = 1 + tb * g.bt;
@@ -348,7 +360,7 @@ __global__ void __launch_bounds__(32) gs2d_lines_kernel(GsArgs g) {
     if (lane < 8) {
       const int p = g.preds[tile * 8 + lane];
       if (p >= 0)
-        spin_flag(g.flags + p);
+        spin_flag(g.flags + p, g.err);
     }
     __syncwarp();
     const int t0 = 1 + tb * BT, x0 = 2 + xb * BX, y0 = 4 + yb * g.by;
@@ -454,6 +466,7 @@ struct PipeArgs {
   int nclk;         // clocks per level (c = -1 .. n + 61)
   long long* prof;  // optional per-warp counters [nb * NW][16] (PCOTGPU_GS_PROF dev aid)
   int spin_ns;      // edge-poll backoff cap (ns)
+  int* err;         // fault word (spin cap hit)
 };
 
 // CTA-scope acquire/release on the shared-memory progress words: the acquire
@@ -472,28 +485,35 @@ PCOT_DEV void st_release_cta(volatile int* p, int v) {
                : "memory");
 }
 
-// Spins are bounded (~tens of seconds): a scheduling bug then shows up as a
-// wrong result in the parity tests instead of a hung device.
+// Spins are bounded (~seconds): a scheduling bug or lost co-residency then
+// sets the fault word (the run fails with an error) instead of hanging the
+// device or returning a silently wrong grid.
 constexpr long long kSpinCap = 40000000LL;
+PCOT_DEV void spin_fault(int* err) {
+  if ((threadIdx.x & 31) == 0) atomicOr(err, 1);
+}
 
 // Waits are executed by the whole warp (every lane reads the same word, one
 // transaction) and exit on a warp vote: a lane-0-only spin leaves the warp
 // diverged and every later shuffle takes the compiler's slow collective path.
-PCOT_DEV void wait_smem(const volatile int* p, int target) {
-  for (long long it = 0; !__all_sync(0xffffffffu, vld(p) >= target) && it < kSpinCap; ++it)
-    __nanosleep(8);
+PCOT_DEV void wait_smem(const volatile int* p, int target, int* err) {
+  long long it = 0;
+  for (; !__all_sync(0xffffffffu, vld(p) >= target) && it < kSpinCap; ++it) __nanosleep(8);
+  if (it == kSpinCap) spin_fault(err);
 }
 
 // Same wait through a per-warp cache of the last value seen: progress words
 // only grow, and an earlier acquire of a value >= target already orders the
 // reads that need it, so a producer running ahead costs no shared load.
-PCOT_DEV void wait_seen(const volatile int* p, int target, int& seen) {
+PCOT_DEV void wait_seen(const volatile int* p, int target, int& seen, int* err) {
   if (seen >= target) return;
   int v = vld(p);
-  for (long long it = 0; !__all_sync(0xffffffffu, v >= target) && it < kSpinCap; ++it) {
+  long long it = 0;
+  for (; !__all_sync(0xffffffffu, v >= target) && it < kSpinCap; ++it) {
     __nanosleep(8);
     v = vld(p);
   }
+  if (it == kSpinCap) spin_fault(err);
   seen = v;
 }
 
@@ -586,12 +606,13 @@ __global__ void __launch_bounds__(NW * 32, 1) gs2d_pipe_kernel(PipeArgs g) {
       const int col = xcol(k);
       const bool mine = xpoll && col >= 0 && col < g.n;
       unsigned ns = 16;
-      for (long long it = 0; __any_sync(0xffffffffu, mine && is_empty(v)) && it < kSpinCap;
-           ++it) {
+      long long it = 0;
+      for (; __any_sync(0xffffffffu, mine && is_empty(v)) && it < kSpinCap; ++it) {
         if (g.spin_ns) __nanosleep(ns);
         ns = ns * 2 < unsigned(g.spin_ns) ? ns * 2 : unsigned(g.spin_ns);
         if (mine && is_empty(v)) v = ld_relaxed(xrow + col);
       }
+      if (it == kSpinCap) spin_fault(g.err);
       if ((xa || xc) && col >= 0 && col < g.n) xring[col & (SG - 1)] = v;
     };
     // warp 0: lane q stages level t-1 row i0 - t + 2 + q (the last warp's
@@ -616,7 +637,7 @@ __global__ void __launch_bounds__(NW * 32, 1) gs2d_pipe_kernel(PipeArgs g) {
     };
     double2 pre[S / 2];  // warp 0: chunk k+1's new pairs, in flight during chunk k
     if (w == 0) {
-      if (t > 1) wait_smem(prog + NW - 1, plvl + need(S - 2 + 2));
+      if (t > 1) wait_smem(prog + NW - 1, plvl + need(S - 2 + 2), g.err);
       store_pair(0, 0, load_pair(0, 0));
 #pragma unroll
       for (int m = 1; m <= S / 2; ++m) pre[m - 1] = load_pair(0, m);
@@ -645,7 +666,7 @@ __global__ void __launch_bounds__(NW * 32, 1) gs2d_pipe_kernel(PipeArgs g) {
 #pragma unroll
         for (int m = 1; m <= S / 2; ++m) store_pair(k, m, pre[m - 1]);
         if (k + 1 < nchunk) {
-          if (t > 1) wait_seen(prog + NW - 1, plvl + need(c_hi + S + 2), seen_wrap);
+          if (t > 1) wait_seen(prog + NW - 1, plvl + need(c_hi + S + 2), seen_wrap, g.err);
           PCOT_PROF(1);
 #pragma unroll
           for (int m = 1; m <= S / 2; ++m) pre[m - 1] = load_pair(k + 1, m);
@@ -654,7 +675,7 @@ __global__ void __launch_bounds__(NW * 32, 1) gs2d_pipe_kernel(PipeArgs g) {
       PCOT_PROF(7);
       // producer ahead: D of clock c is producer lane l's column j+1, computed
       // at the producer's clock c+1
-      if (w > 0) wait_seen(prog + w - 1, plvl + need(c_hi + 2), seen_prod);
+      if (w > 0) wait_seen(prog + w - 1, plvl + need(c_hi + 2), seen_prod, g.err);
       PCOT_PROF(2);
       if (w < NW - 1) {
         // ring reuse: the consumer (level t+1) must have read what this chunk
@@ -663,9 +684,9 @@ __global__ void __launch_bounds__(NW * 32, 1) gs2d_pipe_kernel(PipeArgs g) {
         // t+1, since every slot is written, out-of-range columns included.
         const int rel = c_hi + 1 - (RS - 4);
         if (rel > 0) {
-          if (t + 1 <= g.T) wait_seen(prog + w + 1, clvl + need(rel), seen_cons);
+          if (t + 1 <= g.T) wait_seen(prog + w + 1, clvl + need(rel), seen_cons, g.err);
         } else if (t + 1 - NW >= 1) {
-          wait_seen(prog + w + 1, (t + 1 - NW) * BIG + fin, seen_cons);
+          wait_seen(prog + w + 1, (t + 1 - NW) * BIG + fin, seen_cons, g.err);
         }
       }
       PCOT_PROF(3);
@@ -714,7 +735,9 @@ __global__ void __launch_bounds__(NW * 32, 1) gs2d_pipe_kernel(PipeArgs g) {
         // every column's slot, in range or not: out-of-range slots are only
         // read by consumer cells that are themselves not updated
         myring[(j0 + kk) & (RS - 1)] = v;
-        if ((emask >> kk) & 1u) st_relaxed(ep + kk, v);  // lane 31: the band's last row
+        // lane 31: the band's last row (a computed NaN carrying the kEmpty bit
+        // pattern would read as "not yet written": stored as the canonical NaN)
+        if ((emask >> kk) & 1u) st_relaxed(ep + kk, is_empty(v) ? __longlong_as_double(0x7fffffffffffffffLL) : v);
         if ((omask >> kk) & 1u) op[kk] = v;              // result / wrap buffer
       }
       PCOT_PROF(5);
@@ -767,6 +790,13 @@ GsPlan* gs2d_plan_create(int64_t n, int64_t T, int bt, int bx, int by, int devic
   p->bx = bx;
   p->by = by;
   p->device = device;
+  if (cudaSetDevice(device) != cudaSuccess || cudaMalloc(&p->d_err, sizeof(int)) != cudaSuccess ||
+      cudaMemset(p->d_err, 0, sizeof(int)) != cudaSuccess ||
+      cudaHostAlloc(&p->h_err, sizeof(int), cudaHostAllocDefault) != cudaSuccess) {
+    p->setup_failed = true;
+    return p;
+  }
+  *p->h_err = 0;
   if (T < 1 || n < 3) return p;  // nothing to do
   if (bt == 0) {  // systolic pipeline: every band's CTA must be resident
     p->pipe = true;
@@ -812,23 +842,35 @@ GsPlan* gs2d_plan_create(int64_t n, int64_t T, int bt, int bx, int by, int devic
     preds.insert(preds.end(), pr, pr + 8);
   }
   p->ntiles = int64_t(order.size());
-  cudaSetDevice(device);
-  cudaMalloc(&p->d_tiles, tiles.size() * sizeof(int));
-  cudaMalloc(&p->d_preds, preds.size() * sizeof(int));
-  cudaMalloc(&p->d_state, (p->ntiles + 1) * sizeof(int));
-  cudaMemcpy(p->d_tiles, tiles.data(), tiles.size() * sizeof(int), cudaMemcpyHostToDevice);
-  cudaMemcpy(p->d_preds, preds.data(), preds.size() * sizeof(int), cudaMemcpyHostToDevice);
-  cudaStreamSynchronize(0);  // legacy-stream copies vs the caller's non-blocking stream
   const int ni = bx + bt + 1, ns = by + 2 * bt + 2;
   const int kind = gs_kind(bt, bx);
   const size_t smem = size_t(ni) * ns * (kind ? 9 : 8) + 16;
   auto kern = kind == 2 ? lines::gs2d_lines_kernel : kind == 1 ? gs2d_warp_kernel : gs2d_kernel;
-  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-  int occ = 0, sms = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kind ? 32 : bt * bx, smem);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
-  p->grid = int(std::max<int64_t>(1, std::min<int64_t>(p->ntiles, int64_t(occ) * sms)));
+  int slots = 0;
+  if (cudaMalloc(&p->d_tiles, tiles.size() * sizeof(int)) != cudaSuccess ||
+      cudaMalloc(&p->d_preds, preds.size() * sizeof(int)) != cudaSuccess ||
+      cudaMalloc(&p->d_state, (p->ntiles + 1) * sizeof(int)) != cudaSuccess ||
+      cudaMemcpy(p->d_tiles, tiles.data(), tiles.size() * sizeof(int), cudaMemcpyHostToDevice) != cudaSuccess ||
+      cudaMemcpy(p->d_preds, preds.data(), preds.size() * sizeof(int), cudaMemcpyHostToDevice) != cudaSuccess ||
+      // legacy-stream copies vs the caller's non-blocking stream
+      cudaStreamSynchronize(0) != cudaSuccess ||
+      kernel_slots(reinterpret_cast<const void*>(kern), kind ? 32 : bt * bx, smem, &slots) != cudaSuccess ||
+      slots <= 0) {
+    p->setup_failed = true;
+    return p;
+  }
+  p->grid = int(std::max<int64_t>(1, std::min<int64_t>(p->ntiles, slots)));
   return p;
+}
+
+// Fault word of the last runs (call after synchronising the run's stream):
+// nonzero if a dependence wait hit its spin cap; reading it re-arms it.
+int gs2d_plan_fault(GsPlan* p) {
+  if (!p || !p->h_err || !*p->h_err) return 0;
+  *p->h_err = 0;
+  cudaMemset(p->d_err, 0, sizeof(int));
+  cudaDeviceSynchronize();
+  return 1;
 }
 
 void gs2d_plan_destroy(GsPlan* p) {
@@ -839,6 +881,8 @@ void gs2d_plan_destroy(GsPlan* p) {
   cudaFree(p->wb[0]);
   cudaFree(p->wb[1]);
   cudaFree(p->eb);
+  cudaFree(p->d_err);
+  if (p->h_err) cudaFreeHost(p->h_err);
   delete p;
 }
 
@@ -881,13 +925,13 @@ size_t gs2d_pipe_edge_bytes(int64_t n, int64_t seg) {
 // the free memory, and launches of at least min(T, 64) levels.
 int64_t gs2d_pipe_segment(int64_t n, int64_t T, int device) {
   if (n < 3 || T < 1) return 0;
-  int sms = 0, occ = 0;
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
   const PipeVariant& v = pipe_variant();
   const size_t smem = gs2d_pipe_smem(v);
-  cudaFuncSetAttribute(v.kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, v.kern, v.nw * 32, smem);
-  const int64_t cap = int64_t(occ) * sms;
+  int slots = 0;
+  if (cudaSetDevice(device) != cudaSuccess ||
+      kernel_slots(reinterpret_cast<const void*>(v.kern), v.nw * 32, smem, &slots) != cudaSuccess)
+    return 0;
+  const int64_t cap = slots;
   int64_t seg = std::min<int64_t>(T, 32 * cap - (n - 2) + 1);
   seg = std::min<int64_t>(seg, (int64_t(1) << 31) / pipe::BIG - 2);
   size_t free_b = 0, total_b = 0;
@@ -917,14 +961,13 @@ cudaError_t gs2d_pipe_run(GsPlan* p, double* a, int64_t ld, cudaStream_t stream)
   }
   const PipeVariant& v = pipe_variant();
   const size_t smem = gs2d_pipe_smem(v);
-  if ((e = cudaFuncSetAttribute(v.kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                int(smem))) != cudaSuccess)
+  if ((e = kernel_slots(reinterpret_cast<const void*>(v.kern), v.nw * 32, smem, nullptr)) != cudaSuccess)
     return e;
   for (int64_t t0 = 0; t0 < p->T; t0 += p->seg) {
     const int64_t len = std::min(p->seg, p->T - t0);
     if ((e = gs2d_pipe_launch(p, v, smem, a, ld, len, stream)) != cudaSuccess) return e;
   }
-  return cudaSuccess;
+  return cudaMemcpyAsync(p->h_err, p->d_err, sizeof(int), cudaMemcpyDeviceToHost, stream);
 }
 
 // One launch: `len` levels from the grid in `a` (level 0) back into `a`.
@@ -948,15 +991,28 @@ cudaError_t gs2d_pipe_launch(GsPlan* p, const PipeVariant& v, size_t smem, doubl
   g.nb = nb;
   g.nclk = int(p->n) + 63;
   g.prof = nullptr;
-  const char* sp = getenv("PCOTGPU_GS_SPIN");
-  g.spin_ns = sp ? atoi(sp) : 256;
+  g.err = p->d_err;
+  g.spin_ns = env_int("PCOTGPU_GS_SPIN", 256);
   const char* pe = getenv("PCOTGPU_GS_PROF");  // development aid: cycle breakdown
   const size_t np = size_t(nb) * v.nw * 16;
   if (pe && atoi(pe)) {
     if ((e = cudaMalloc(&g.prof, np * 8)) != cudaSuccess) return e;
     cudaMemsetAsync(g.prof, 0, np * 8, stream);
   }
-  v.kern<<<nb, v.nw * 32, smem, stream>>>(g);
+  // Every band's CTA must be resident (bands wait on the band above):
+  // cooperative launch makes that a launch-time guarantee — it fails with
+  // cudaErrorCooperativeLaunchTooLarge instead of deadlocking.
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(nb);
+  cfg.blockDim = dim3(v.nw * 32);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  if ((e = cudaLaunchKernelEx(&cfg, v.kern, g)) != cudaSuccess) return e;
   count_launch();
   if (g.prof) {
     std::vector<long long> h(np);
@@ -1026,6 +1082,7 @@ cudaError_t div9_check(const double* x, double* q_fast, double* q_ref, int64_t n
 }
 
 cudaError_t gs2d_run(GsPlan* p, double* a, int64_t ld, cudaStream_t stream) {
+  if (p->setup_failed) return cudaErrorMemoryAllocation;
   if (p->pipe) return gs2d_pipe_run(p, a, ld, stream);
   if (p->ntiles == 0) return cudaSuccess;
   cudaError_t e = cudaMemsetAsync(p->d_state, 0, (p->ntiles + 1) * sizeof(int), stream);
@@ -1045,6 +1102,7 @@ cudaError_t gs2d_run(GsPlan* p, double* a, int64_t ld, cudaStream_t stream) {
   g.preds = p->d_preds;
   g.flags = p->d_state;
   g.counter = p->d_state + p->ntiles;
+  g.err = p->d_err;
   const int kind = gs_kind(p->bt, p->bx);
   const size_t smem = size_t(g.ni) * g.ns * (kind ? 9 : 8) + 16;
   if (kind == 2)
@@ -1054,7 +1112,8 @@ cudaError_t gs2d_run(GsPlan* p, double* a, int64_t ld, cudaStream_t stream) {
   else
     gs2d_kernel<<<p->grid, p->bt * p->bx, smem, stream>>>(g);
   count_launch();
-  return cudaGetLastError();
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  return cudaMemcpyAsync(p->h_err, p->d_err, sizeof(int), cudaMemcpyDeviceToHost, stream);
 }
 
 }  // namespace pcotgpu

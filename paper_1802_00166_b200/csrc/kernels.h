@@ -60,6 +60,9 @@ bool gs2d_pipe_fits(int64_t n, int64_t T, int device);
 void gs2d_plan_destroy(GsPlan* p);
 cudaError_t gs2d_run(GsPlan* p, double* a, int64_t ld, cudaStream_t stream);
 int64_t gs2d_plan_tiles(const GsPlan* p);
+// Nonzero if a dependence wait of the runs since the last call hit its spin
+// cap (the grid is then invalid); call after synchronising the run's stream.
+int gs2d_plan_fault(GsPlan* p);
 // Test hook: the Gauss-Seidel kernel's x/9 vs the IEEE division, elementwise.
 cudaError_t div9_check(const double* x, double* q_fast, double* q_ref, int64_t n,
                        cudaStream_t stream);
@@ -84,6 +87,14 @@ cudaError_t copy_rows(double* dst, int64_t ldd, const double* src, int64_t lds, 
 // Zero (or keep) the ring of a 2-D grid: cells on rows 0/N-1, cols 0/N-1.
 cudaError_t zero_ring_2d(double* origin, int64_t ld, int64_t n, cudaStream_t stream);
 cudaError_t zero_ring_3d(const Grid3D& g, cudaStream_t stream);
+
+// Per-(kernel, device) launch preparation, thread-safe and cached: sets the
+// dynamic shared-memory opt-in for `smem` on the current device and returns the
+// number of CTAs of `nthreads` that can be resident at once (occupancy x SMs;
+// 0 if none fits).
+cudaError_t kernel_slots(const void* fn, int nthreads, size_t smem, int* slots);
+// Integer environment override (read on every call: cheap, no shared state).
+int env_int(const char* name, int dflt);
 
 // Launch counter (every kernel launched by this library increments it).
 uint64_t launches();

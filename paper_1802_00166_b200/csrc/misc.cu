@@ -1,6 +1,10 @@
 // Device utilities: the reference's deterministic input generator, pitched
 // copies, ring reset, and the launch counter.
 #include <atomic>
+#include <cstdlib>
+#include <map>
+#include <mutex>
+#include <tuple>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -123,6 +127,42 @@ cudaError_t zero_ring_3d(const Grid3D& g, cudaStream_t stream) {
   zero_ring3d_kernel<<<grid_for(g.n * g.n * g.n), 256, 0, stream>>>(g);
   count_launch();
   return cudaGetLastError();
+}
+
+// One-time per (kernel, device, block, smem) preparation, thread-safe: the
+// dynamic shared-memory opt-in is a per-device function attribute, so a
+// process driving several devices (or several host threads) must not share a
+// single "done" flag.
+cudaError_t kernel_slots(const void* fn, int nthreads, size_t smem, int* slots) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  using Key = std::tuple<const void*, int, int, size_t>;
+  static std::mutex mu;
+  static std::map<Key, int> cache;
+  const Key key{fn, dev, nthreads, smem};
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = cache.find(key);
+  if (it != cache.end()) {
+    if (slots) *slots = it->second;
+    return cudaSuccess;
+  }
+  if ((e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem))) !=
+      cudaSuccess)
+    return e;
+  int occ = 0, sms = 0;
+  if ((e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess) return e;
+  if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, nthreads, smem)) != cudaSuccess)
+    return e;
+  const int s = occ * sms;  // 0 when the kernel cannot be resident at all
+  cache[key] = s;
+  if (slots) *slots = s;
+  return cudaSuccess;
+}
+
+int env_int(const char* name, int dflt) {
+  const char* v = std::getenv(name);
+  return v && *v ? std::atoi(v) : dflt;
 }
 
 }  // namespace pcotgpu

@@ -930,8 +930,22 @@ Recognized recognize_gemm(const KernelSpec& k, const IntVec& prm) {
   }
   R.temp = tmp->name;
   R.output = out->name;
+  if (!tmp || !out) unsupported("gemm needs one temp and one output array");
   std::string upd;
   const size_t nidx = k.indices.size();
+  int nfinal = 0, ninit = 0, nupdate = 0;
+  // canonical form of a statement's write reference (same notation as reads)
+  auto write_ref = [&](const Statement& s) {
+    auto e = std::make_shared<Expr>();
+    e->kind = Expr::Kind::Read;
+    e->array = s.write_array;
+    e->subs = s.write_subs;
+    int nr = 0;
+    std::string c = canon_plain(e, nidx, nr);
+    c = replace_all(c, tmp->name + "[", "C[");
+    return replace_all(c, out->name + "[", "Out[");
+  };
+  const std::string kTmpIJK = "C[+1*$0,+1*$1,+1*$2]";
   for (const auto& s : k.statements) {
     StmtBox b;
     b.id = s.id;
@@ -949,10 +963,18 @@ Recognized recognize_gemm(const KernelSpec& k, const IntVec& prm) {
     std::string c = canon_plain(s.body, nidx, nr);
     if (s.write_array == out->name) {
       b.role = "final";
+      ++nfinal;
+      // Out[i, j] = C[i, j, k] (at k = N): a plain copy, identity subscripts
+      if (write_ref(s) != "Out[+1*$0,+1*$1]" || replace_all(c, tmp->name + "[", "C[") != kTmpIJK)
+        unsupported("gemm output statement is not Out[i,j] = C[i,j,k]");
     } else if (s.body->kind == Expr::Kind::Lit && s.body->lit == 0.0) {
       b.role = "init";
+      ++ninit;
+      if (write_ref(s) != kTmpIJK) unsupported("gemm init statement does not write C[i,j,k]");
     } else {
       b.role = "update";
+      ++nupdate;
+      if (write_ref(s) != kTmpIJK) unsupported("gemm update statement does not write C[i,j,k]");
       upd = c;
       // A/B are the two inputs in declaration order: substitute their names
       if (ins.size() != 2) unsupported("gemm needs two inputs");
@@ -962,6 +984,8 @@ Recognized recognize_gemm(const KernelSpec& k, const IntVec& prm) {
     }
     R.stmts.push_back(b);
   }
+  if (nfinal != 1 || ninit != 1 || nupdate != 1)
+    unsupported("gemm needs exactly one init, one update and one output statement");
   if (upd != kGEMM) unsupported("update body not in the registry: " + upd);
   const StmtBox* fb = nullptr;
   for (const auto& b : R.stmts)

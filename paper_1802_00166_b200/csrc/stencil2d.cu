@@ -27,14 +27,7 @@
 namespace pcotgpu {
 
 // PCOTGPU_PDL=0 turns programmatic dependent launch off (A/B measurements).
-bool pdl_enabled() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = std::getenv("PCOTGPU_PDL");
-    v = e && e[0] == '0' ? 0 : 1;
-  }
-  return v == 1;
-}
+bool pdl_enabled() { return env_int("PCOTGPU_PDL", 1) != 0; }
 
 namespace {
 
@@ -425,25 +418,13 @@ cudaError_t launch_cfg(S2Args a, int ring_hold, int rows, cudaStream_t stream) {
   constexpr int kPF = ring_depth<MINB>();
   constexpr size_t smem = size_t(kPF) * (NT * C + 2) * 8 +
                           size_t(EdgeLayout<BT, NT, XS>::kDoubles) * 8 + size_t(kPF) * 8;
-  static int slots[2] = {0, 0};
-  int& sl = slots[ring_hold ? 1 : 0];
-  if (sl == 0) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    if (e != cudaSuccess) return e;
-    int occ = 0, sms = 0, dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, NT, smem);
-    sl = (occ > 0 ? occ : 1) * (sms > 0 ? sms : 148);
-  }
+  int sl = 0;
+  if (cudaError_t e = kernel_slots(reinterpret_cast<const void*>(kern), NT, smem, &sl)) return e;
+  if (sl <= 0) return cudaErrorInvalidConfiguration;
   a.w_out = NT * C - 2 * BT;
   a.nstrips = int((a.cols + (BT & 1) + a.w_out - 1) / a.w_out);
   size_grid(a, BT, rows, sl);
-  static int force_chunks = -1;  // PCOTGPU_S2D5_CHUNKS: tuning override of the row chunking
-  if (force_chunks < 0) {
-    const char* v = std::getenv("PCOTGPU_S2D5_CHUNKS");
-    force_chunks = v ? std::atoi(v) : 0;
-  }
+  const int force_chunks = env_int("PCOTGPU_S2D5_CHUNKS", 0);  // tuning override of the row chunking
   if (force_chunks > 0 && force_chunks <= rows) {
     a.nchunks = force_chunks;
     a.H = (rows + force_chunks - 1) / force_chunks;
@@ -456,9 +437,7 @@ cudaError_t launch_cfg(S2Args a, int ring_hold, int rows, cudaStream_t stream) {
   } else {
     grid = a.nstrips * a.nchunks;
   }
-  static int dbg = -1;
-  if (dbg < 0) dbg = std::getenv("PCOTGPU_S2D5_DEBUG") ? 1 : 0;
-  if (dbg)
+  if (env_int("PCOTGPU_S2D5_DEBUG", 0))
     std::fprintf(stderr, "s2d5 bt=%d C=%d NT=%d slots=%d strips=%d chunks=%d H=%d grid=%d\n", BT, C,
                  NT, sl, a.nstrips, a.nchunks, a.H, grid);
   // Programmatic dependent launch: back-to-back depth blocks overlap one
@@ -551,11 +530,7 @@ cudaError_t s2d5_advance_p2p(const Slab2D& in, const Slab2D& out, int64_t g0, in
   a.mir_dn = mirror_rows > 0 ? mirror_dn : nullptr;
   a.mir_lo = mirror_rows;
   a.mir_hi = out.rows - mirror_rows;
-  static int variant = -2;
-  if (variant == -2) {
-    const char* v = std::getenv("PCOTGPU_S2D5_VARIANT");
-    variant = v ? std::atoi(v) : -1;  // -1: automatic per depth
-  }
+  const int variant = env_int("PCOTGPU_S2D5_VARIANT", -1);  // -1: automatic per depth
   const int rows = row_hi - row_lo;
 #ifdef PCOT_S2_DEV_BT  // development: instantiate one depth only (fast SASS checks)
   return bt == PCOT_S2_DEV_BT ? launch_bt<PCOT_S2_DEV_BT>(a, ring_hold, rows, variant, stream)

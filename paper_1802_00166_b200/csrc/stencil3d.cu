@@ -31,14 +31,7 @@ namespace pcotgpu {
 namespace {
 
 // PCOTGPU_S3D7_CHUNKS: tuning override of the plane chunking (tools/kbench.py s3d7)
-int forced_chunks() {
-  static int fc = -1;
-  if (fc < 0) {
-    const char* v = std::getenv("PCOTGPU_S3D7_CHUNKS");
-    fc = v ? std::atoi(v) : 0;
-  }
-  return fc;
-}
+int forced_chunks() { return env_int("PCOTGPU_S3D7_CHUNKS", 0); }
 
 template <int C_, int RJ_, int NW_, int MINB_, int PF_>
 struct Geo {
@@ -299,16 +292,9 @@ cudaError_t launch3(S3Args a, cudaStream_t stream) {
   constexpr size_t smem = size_t(G::PF) * G::JW * G::KL * 8 +
                           size_t(2) * Edge3<BT, G>::kPerPar * 8 + G::PF * 8;
   auto fn = s3d7_kernel<BT, RULE, HOLD, G>;
-  static int slots = 0;
-  if (slots == 0) {
-    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    if (e != cudaSuccess) return e;
-    int occ = 0, sms = 0, dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, G::NT, smem);
-    slots = (occ > 0 ? occ : 1) * (sms > 0 ? sms : 148);
-  }
+  int slots = 0;
+  if (cudaError_t e = kernel_slots(reinterpret_cast<const void*>(fn), G::NT, smem, &slots)) return e;
+  if (slots <= 0) return cudaErrorInvalidConfiguration;
   a.kout = G::KW - 2 * BT;
   a.jout = G::JW - 2 * BT;
   a.nk = (a.n + a.kout - 1) / a.kout;
@@ -720,14 +706,15 @@ __global__ void __launch_bounds__(G::NT, G::MINB)
 
 // 3-D tensor map over the whole padded input cube (halo included), box KL x JL x 1.
 cudaError_t encode_plane_map(CUtensorMap* m, const S3Args& a, int kl, int jl) {
-  static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
-  if (!encode) {
+  static const PFN_cuTensorMapEncodeTiled_v12000 encode = [] {  // thread-safe one-time lookup
     cudaDriverEntryPointQueryResult q;
     void* fn = nullptr;
     cudaError_t e = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q);
-    if (e != cudaSuccess || q != cudaDriverEntryPointSuccess || !fn) return cudaErrorNotSupported;
-    encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
-  }
+    return (e == cudaSuccess && q == cudaDriverEntryPointSuccess)
+               ? reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn)
+               : nullptr;
+  }();
+  if (!encode) return cudaErrorNotSupported;
   const double* base = a.in - int64_t(a.halo) * (a.pi_in + a.pj_in + 1);
   const cuuint64_t dims[3] = {cuuint64_t(a.pj_in), cuuint64_t(a.pi_in / a.pj_in),
                               cuuint64_t(a.n + 2 * a.halo)};
@@ -745,16 +732,9 @@ cudaError_t launch3v2(S3Args a, cudaStream_t stream) {
   constexpr size_t smem = size_t(G::PF) * G::SLOT * 8 +
                           size_t(2) * Edge3v2<BT, G>::kPerPar * 8 + G::PF * 8;
   auto fn = s3d7v2_kernel<BT, RULE, HOLD, G>;
-  static int slots = 0;
-  if (slots == 0) {
-    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    if (e != cudaSuccess) return e;
-    int occ = 0, sms = 0, dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, G::NT, smem);
-    slots = (occ > 0 ? occ : 1) * (sms > 0 ? sms : 148);
-  }
+  int slots = 0;
+  if (cudaError_t e = kernel_slots(reinterpret_cast<const void*>(fn), G::NT, smem, &slots)) return e;
+  if (slots <= 0) return cudaErrorInvalidConfiguration;
   a.kout = G::KW - 2 * BT;
   a.jout = G::JW - 2 * BT;
   a.nk = (a.n + (BT & 1) + a.kout - 1) / a.kout;
@@ -864,11 +844,7 @@ cudaError_t s3d7_advance(const Grid3D& in, const Grid3D& out, int bt, int rule, 
   a.pi_out = out.pitch_i;
   a.halo = int(in.halo);
   a.order = order;
-  static int variant = -2;
-  if (variant == -2) {
-    const char* v = std::getenv("PCOTGPU_S3D7_VARIANT");
-    variant = v ? std::atoi(v) : -1;
-  }
+  const int variant = env_int("PCOTGPU_S3D7_VARIANT", -1);
   switch (bt) {
     case 1: return launch3_bt<1>(a, rule, ring_hold, variant, stream);
     case 2: return launch3_bt<2>(a, rule, ring_hold, variant, stream);

@@ -128,10 +128,17 @@ BIG = [
     ("gemm", {"N": 1000}, (32, 32, 32)),
 ]
 
+# BASELINE config 4 at full size (32768^2, T=512): the emitted C needs ~34 GB of
+# host RAM and ~20-30 min on 8 cores, so it runs only on request (--cfg4).
+HUGE = [
+    ("jacobi2d", {"T": 512, "N": 32768}, (16, 128, 1024)),
+]
+
 
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--big", action="store_true", help="also run the emitted-C goldens")
+    ap.add_argument("--cfg4", action="store_true", help="also run config 4 at full size (~34 GB RAM)")
     args = ap.parse_args()
     if not os.path.exists(REF_BIN):
         sys.exit("build the reference first: make -C oracle")
@@ -179,6 +186,17 @@ def main():
         if not args.big:
             continue
         chk = run_emitted(name, params, leaf)
+        entries.append({"kernel": name, "params": params, "checksum": chk,
+                        "source": "reference emitted C (emit_c use_alloc, -O2 "
+                                  "-ffp-contract=off -fopenmp), leaf %s" % list(leaf)})
+        print(name, params, chk, flush=True)
+    for name, params, leaf in HUGE:
+        key = (name, pstr(params))
+        if not args.cfg4:
+            if key in old:
+                entries.append(old[key])
+            continue
+        chk = run_emitted(name, params, leaf, threads=os.cpu_count() or 8)
         entries.append({"kernel": name, "params": params, "checksum": chk,
                         "source": "reference emitted C (emit_c use_alloc, -O2 "
                                   "-ffp-contract=off -fopenmp), leaf %s" % list(leaf)})

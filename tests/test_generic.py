@@ -100,3 +100,36 @@ def test_interpreter_input_from_host_and_errors():
         with pytest.raises(P.PcotError) as err:
             ex.run_untiled()
         assert err.value.kind == "Validation"
+
+
+# Reads that the reference's order serves from a cell's OLD value (the reading
+# statement's own write, or a write by a later point).  Checksums from the
+# unmodified reference (`pcot_ref run <k> N=8 --scheme untiled`; its shadow
+# oracle also flags the kernels as violating, which the reference reports
+# instead of rejecting).  The dataflow grid would wait for those writes; the
+# interpreter must detect the order and run them sequentially.
+ORDER_CASES = [("selfread", "84f9cec8af7cb928"), ("futureread", "de90f9ad18f16e28")]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name,want", ORDER_CASES)
+def test_interpreter_read_before_write_runs_in_reference_order(name, want):
+    import time
+
+    path = os.path.join(O.REPO, "tests", "kernels_extra", name + ".kernel")
+    with P.GpuExecutor(path, {"N": 8}) as ex:
+        t0 = time.perf_counter()
+        r = ex.run_untiled()
+        assert time.perf_counter() - t0 < 5.0  # no dependence wait until a spin cap
+        assert r.checksum_hex == want
+        assert (r.points, r.reads, r.writes) == (8, 16, 8)
+
+
+@pytest.mark.skipif(not os.path.exists(REF_BIN), reason="reference driver not built (oracle/_ref)")
+@pytest.mark.parametrize("name,want", ORDER_CASES)
+def test_read_before_write_goldens_match_reference(name, want):
+    path = os.path.join(O.REPO, "tests", "kernels_extra", name + ".kernel")
+    out = subprocess.run([REF_BIN, "run", path, "N=8", "--scheme", "untiled"],
+                         capture_output=True, text=True, timeout=60)
+    kv = dict(l.split(" ", 1) for l in out.stdout.strip().splitlines())
+    assert kv["CHECKSUM"] == want

@@ -138,13 +138,26 @@ def test_gemm_tolerance(N, scheme):
         _gemm_check(ex.array_data("Out"), N)
 
 
-def test_gemm_config3_rows():
+@pytest.mark.parametrize("scheme", ["untiled", "slt"])
+def test_gemm_config3_all_rows(scheme):
+    """BASELINE config 3 (N=4096): every one of the 4096 rows against the
+    sequential-k oracle (all host threads), normwise and componentwise 1e-12;
+    and the reference's own sampled cells (its emitted-C dump)."""
+    import json
+    import os
+
     N = 4096
     with P.GpuExecutor("gemm", {"N": N}) as ex:
-        ex.run_untiled(skip_checksum=True)
+        ex.run(scheme, None if scheme == "untiled" else [64, 64, 64], skip_checksum=True)
         out = ex.array_data("Out")
-    for rows in [(0, 24), (2040, 2056), (4072, 4096)]:
-        _gemm_check(out, N, rows)
+    O.lib().oracle_set_threads(os.cpu_count() or 1)
+    _gemm_check(out, N)
+    with open(os.path.join(O.REPO, "tests", "golden", "gemm4096_samples.json")) as f:
+        g = json.load(f)
+    rows = np.arange(N)
+    got = out.reshape(N, N)[rows, (rows * 2654435761 + 12345) % N]
+    ref = np.array([int(h, 16) for h in g["out_hex"]], dtype=np.uint64).view(np.float64)
+    assert (np.abs(got - ref) / np.array(g["absab"])).max() <= 1e-12
 
 
 def test_storage_persists_and_reset():
@@ -208,6 +221,17 @@ def test_config4_full_size_windows_and_ring():
         ex.run_untiled(skip_checksum=True)
         out2 = ex.array_data("Out").reshape(N, N)
         assert np.array_equal(out2[:64, :64], corner * 2.0)
+
+
+@pytest.mark.slow
+def test_config4_full_size_checksum():
+    """BASELINE config 4 (32768^2, T=512): the FNV-1a checksum of the whole
+    8 GiB output equals the reference's (its emitted C at full size,
+    tests/golden/make_golden.py --cfg4), for the default and the COT order."""
+    want = _golden("jacobi2d", T=512, N=32768)
+    with P.GpuExecutor("jacobi2d", {"T": 512, "N": 32768}) as ex:
+        assert ex.run_untiled().checksum_hex == want
+        assert ex.run("cot", [8, 64, 256]).checksum_hex == want
 
 
 @pytest.mark.parametrize("kernel,params,tile", [
