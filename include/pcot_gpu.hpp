@@ -42,13 +42,11 @@ struct ExecResult {
   uint64_t launches = 0;
 };
 
-// reference memalloc.hpp:14-33 (accepted for signature parity; the device
-// layout is the executor's own: ping-pong slabs / in-place grids)
-struct MemoryMap {
-  std::string array;
-  IntVec extents;
-  IntVec moduli;
-};
+// MemoryMap: reference memalloc.hpp:14-33 (declared in spec.h).  Maps the
+// hand-written kernels' device layouts reproduce (identity inputs/outputs,
+// the temp single-assignment or folded along a multiple of the kernel's
+// occupancy vector: allocate()'s maps) keep the hot path; any other map set
+// runs on the device interpreter with storage laid out by the maps.
 
 class GpuExecutor {
  public:

@@ -77,6 +77,21 @@ typedef struct {
   uint64_t launches; /* kernels launched by this run */
 } pcotgpu_result;
 
+/* MemoryMap (reference memalloc.hpp:14-33) of one array:
+ *   storage_k = (sum_c linear[k * rank + c] * cell_c + constant[k]) mod moduli[k]
+ * (moduli[k] == 0: no modulo), storage_k in [0, extents[k]), row-major. */
+typedef struct {
+  const char* array;
+  int32_t rank;            /* the array's (cell) rank */
+  int32_t storage_rank;    /* entries of constant / moduli / extents */
+  const int64_t* linear;   /* storage_rank x rank, row-major */
+  const int64_t* constant;
+  const int64_t* moduli;
+  const int64_t* extents;
+  int32_t single_assignment;
+  int32_t reserved;
+} pcotgpu_map;
+
 typedef struct pcotgpu_handle pcotgpu_handle;
 
 /* ---- registration (host only; no GPU needed) ---------------------------- */
@@ -87,11 +102,27 @@ int pcotgpu_recognize(const char* kernel_json, const int64_t* params, size_t npa
  * ./kernels); writes "" when not found. */
 int pcotgpu_find_kernel_file(const char* name_or_path, char* out, size_t cap);
 
+/* Host only: the map checks pcotgpu_create_mapped makes (one map per array,
+ * arities; Validation for out-of-extent storage) and whether the hand-written
+ * kernel keeps the run (*hot_path = 1) or the interpreter takes it (0); `why`
+ * (may be NULL) receives the reason the hot path declined. */
+int pcotgpu_check_maps(const char* kernel_json, const int64_t* params, size_t nparams,
+                       const pcotgpu_map* maps, size_t nmaps, int* hot_path, char* why, size_t cap);
+
 /* ---- Executor ------------------------------------------------------------ */
 /* Executor(p, params, maps) — exec.hpp:64.  Allocates device storage and
  * initialises inputs with init_value (exec.cpp:21-28, 281-294). */
 int pcotgpu_create(const char* kernel_json, const int64_t* params, size_t nparams, int device,
                    pcotgpu_handle** out);
+/* Executor(p, params, maps) with the caller's memory maps (one per array, as
+ * the reference requires: exec.cpp:134-141).  The hand-written kernels run
+ * when their device layout reproduces the reference's storage semantics
+ * (inputs/outputs: identity at the declared extents; the temp: single
+ * assignment, or folded along a multiple of the kernel's occupancy vector —
+ * what allocate() derives); any other map set runs on the device interpreter
+ * with storage laid out exactly by the maps.  Out-of-extent maps: Validation. */
+int pcotgpu_create_mapped(const char* kernel_json, const int64_t* params, size_t nparams,
+                          const pcotgpu_map* maps, size_t nmaps, int device, pcotgpu_handle** out);
 /* Executor::run(order, opts) — exec.hpp:71; sched == NULL means untiled. */
 int pcotgpu_run(pcotgpu_handle* h, const pcotgpu_schedule* sched, pcotgpu_result* res);
 /* Executor::run_untiled — exec.hpp:73. */

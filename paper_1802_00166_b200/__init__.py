@@ -13,7 +13,7 @@ import numpy as np
 
 __all__ = [
     "lib", "PcotError", "KernelInfo", "ExecResult", "GpuExecutor", "recognize",
-    "find_kernel_file", "load_kernel_text", "fnv1a", "FAMILIES", "SCHEMES",
+    "find_kernel_file", "load_kernel_text", "fnv1a", "FAMILIES", "SCHEMES", "check_maps",
 ]
 
 PKG = os.path.dirname(os.path.abspath(__file__))
@@ -49,6 +49,14 @@ class KernelInfo(ctypes.Structure):
         return FAMILIES.get(self.family, "?")
 
 
+class MapC(ctypes.Structure):
+    """pcotgpu_map: reference MemoryMap (memalloc.hpp:14-33)."""
+    _fields_ = [("array", ctypes.c_char_p), ("rank", ctypes.c_int32), ("storage_rank", ctypes.c_int32),
+                ("linear", ctypes.POINTER(ctypes.c_int64)), ("constant", ctypes.POINTER(ctypes.c_int64)),
+                ("moduli", ctypes.POINTER(ctypes.c_int64)), ("extents", ctypes.POINTER(ctypes.c_int64)),
+                ("single_assignment", ctypes.c_int32), ("reserved", ctypes.c_int32)]
+
+
 class Schedule(ctypes.Structure):
     _fields_ = [("scheme", ctypes.c_int32), ("ndim", ctypes.c_int32),
                 ("leaf", ctypes.c_int64 * 8), ("flags", ctypes.c_int32),
@@ -76,6 +84,11 @@ _SIGS = [
     ("pcotgpu_recognize", ctypes.c_int, [ctypes.c_char_p, _I64P, ctypes.c_size_t, ctypes.POINTER(KernelInfo)]),
     ("pcotgpu_find_kernel_file", ctypes.c_int, [ctypes.c_char_p, ctypes.c_char_p, ctypes.c_size_t]),
     ("pcotgpu_create", ctypes.c_int, [ctypes.c_char_p, _I64P, ctypes.c_size_t, ctypes.c_int, ctypes.POINTER(ctypes.c_void_p)]),
+    ("pcotgpu_create_mapped", ctypes.c_int, [ctypes.c_char_p, _I64P, ctypes.c_size_t, ctypes.POINTER(MapC),
+                                             ctypes.c_size_t, ctypes.c_int, ctypes.POINTER(ctypes.c_void_p)]),
+    ("pcotgpu_check_maps", ctypes.c_int, [ctypes.c_char_p, _I64P, ctypes.c_size_t, ctypes.POINTER(MapC),
+                                          ctypes.c_size_t, ctypes.POINTER(ctypes.c_int), ctypes.c_char_p,
+                                          ctypes.c_size_t]),
     ("pcotgpu_run", ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(Schedule), ctypes.POINTER(ExecResult)]),
     ("pcotgpu_run_untiled", ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(ExecResult)]),
     ("pcotgpu_run_batch", ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(Schedule), ctypes.c_size_t,
@@ -180,6 +193,33 @@ def _params_array(text, params):
     return (ctypes.c_int64 * max(1, len(vals)))(*vals), len(vals)
 
 
+def _maps_array(maps):
+    """maps: [{"array", "linear" (rows), "constant", "moduli", "extents"}] ->
+    (ctypes array of MapC, keep-alive list)."""
+    keep = []
+    arr = (MapC * max(1, len(maps)))()
+    for i, m in enumerate(maps):
+        lin = [v for row in m["linear"] for v in row]
+        rank = len(m["linear"][0]) if m["linear"] else 0
+        bufs = [(ctypes.c_int64 * max(1, len(x)))(*x) for x in (lin, m["constant"], m["moduli"], m["extents"])]
+        name = m["array"].encode()
+        keep += bufs + [name]
+        arr[i] = MapC(name, rank, len(m["extents"]), bufs[0], bufs[1], bufs[2], bufs[3],
+                      int(bool(m.get("single_assignment", False))), 0)
+    return arr, keep
+
+
+def check_maps(kernel, params, maps):
+    """Host only: (hot_path, why) for a map set (pcotgpu_check_maps)."""
+    text = load_kernel_text(kernel)
+    arr, n = _params_array(text, params)
+    marr, keep = _maps_array(maps)
+    hot = ctypes.c_int()
+    why = ctypes.create_string_buffer(512)
+    _check(lib().pcotgpu_check_maps(text.encode(), arr, n, marr, len(maps), ctypes.byref(hot), why, 512))
+    return bool(hot.value), why.value.decode()
+
+
 def recognize(kernel, params):
     """parse_kernel + recognizer (host only): returns KernelInfo."""
     text = load_kernel_text(kernel)
@@ -197,13 +237,18 @@ class GpuExecutor:
     TileSpec leaf vector: leaf[0] (time) is the temporal block depth.
     """
 
-    def __init__(self, kernel, params, device=0):
+    def __init__(self, kernel, params, device=0, maps=None):
         self._h = None
         text = load_kernel_text(kernel)
         self.spec = json.loads(text)
         arr, n = _params_array(text, params)
         h = ctypes.c_void_p()
-        _check(lib().pcotgpu_create(text.encode(), arr, n, int(device), ctypes.byref(h)))
+        if maps is None:
+            _check(lib().pcotgpu_create(text.encode(), arr, n, int(device), ctypes.byref(h)))
+        else:  # Executor(p, params, maps): the reference's MemoryMaps
+            marr, keep = _maps_array(maps)
+            _check(lib().pcotgpu_create_mapped(text.encode(), arr, n, marr, len(maps), int(device),
+                                               ctypes.byref(h)))
         self._h = h
         self.info = KernelInfo()
         _check(lib().pcotgpu_info(self._h, ctypes.byref(self.info)))

@@ -59,6 +59,7 @@ struct DevBuf {
 struct GpuExecutor::Impl {
   KernelSpec spec;
   IntVec params;
+  std::vector<MemoryMap> maps;  // the caller's (empty: device layouts / dense)
   Recognized rec;
   int device = 0;
   cudaStream_t stream = nullptr;
@@ -161,7 +162,7 @@ struct GpuExecutor::Impl {
     n = rec.N;
     T = rec.T;
     if (generic) {
-      gplan = generic_plan_create(spec, params, device);
+      gplan = generic_plan_create(spec, params, maps, device);
       rec = Recognized();
       rec.family = Family::Generic;
       rec.ndim = 0;
@@ -617,10 +618,11 @@ struct GpuExecutor::Impl {
 GpuExecutor::GpuExecutor(const KernelSpec& embedded, const IntVec& params,
                          const std::vector<MemoryMap>& maps, int device)
     : impl_(new Impl) {
-  (void)maps;
   impl_->spec = embedded;
   impl_->params = params;
   impl_->device = device;
+  if (!maps.empty()) check_maps(embedded, maps);  // reference map_of / build_ref checks
+  impl_->maps = maps;
   // Hot-path kernels go to their hand-written kernels; anything else the
   // reference can run goes to the device interpreter (generic.h).
   try {
@@ -632,6 +634,13 @@ GpuExecutor::GpuExecutor(const KernelSpec& embedded, const IntVec& params,
     impl_->generic = true;
   }
   if (env_int("PCOTGPU_FORCE_GENERIC", 0)) impl_->generic = true;
+  // Caller maps: the hand-written kernels only where their layout reproduces
+  // the reference's storage semantics; otherwise the interpreter, which lays
+  // storage out by the maps themselves.
+  if (!impl_->generic && !maps.empty()) {
+    std::string why;
+    if (!hot_path_honours(impl_->rec, embedded, params, maps, &why)) impl_->generic = true;
+  }
   impl_->setup();
 }
 
@@ -658,7 +667,10 @@ uint64_t GpuExecutor::array_base(const std::string& a) const {
   uint64_t base = 64;
   for (const auto& d : impl_->spec.arrays) {
     if (d.name == a) return base;
-    base += (impl_->words_of(d.name) * 8 + 63) / 64 * 64;
+    uint64_t w = impl_->words_of(d.name);
+    for (const auto& m : impl_->maps)  // storage words of the caller's maps
+      if (m.array == d.name) w = uint64_t(m.words());
+    base += (w * 8 + 63) / 64 * 64;
   }
   fail(ErrorKind::Validation, "array_base: unknown array " + a);
 }
@@ -821,6 +833,67 @@ int pcotgpu_create(const char* kernel_json, const int64_t* params, size_t nparam
     auto h = std::make_unique<pcotgpu_handle>();
     h->ex = std::make_unique<GpuExecutor>(k, IntVec(params, params + nparams),
                                           std::vector<MemoryMap>{}, device);
+    *out = h.release();
+  });
+}
+
+namespace {
+std::vector<MemoryMap> maps_of(const pcotgpu_map* maps, size_t nmaps) {
+    std::vector<MemoryMap> mm;
+    for (size_t i = 0; i < nmaps; ++i) {
+      const pcotgpu_map& c = maps[i];
+      if (!c.array || c.rank < 0 || c.storage_rank < 0 ||
+          (c.storage_rank && (!c.constant || !c.moduli || !c.extents || (c.rank && !c.linear))))
+        fail(ErrorKind::Validation, "pcotgpu_create_mapped: malformed map " + std::to_string(i));
+      MemoryMap m;
+      m.array = c.array;
+      for (int32_t q = 0; q < c.storage_rank; ++q) {
+        m.linear.emplace_back(c.linear + size_t(q) * c.rank, c.linear + size_t(q + 1) * c.rank);
+        m.constant.push_back(c.constant[q]);
+        m.moduli.push_back(c.moduli[q]);
+        m.extents.push_back(c.extents[q]);
+      }
+      m.single_assignment = c.single_assignment != 0;
+      mm.push_back(std::move(m));
+    }
+    return mm;
+}
+}  // namespace
+
+int pcotgpu_check_maps(const char* kernel_json, const int64_t* params, size_t nparams,
+                       const pcotgpu_map* maps, size_t nmaps, int* hot_path, char* why, size_t cap) {
+  return guarded([&] {
+    if (!kernel_json || !hot_path || (nmaps && !maps)) fail(ErrorKind::Validation, "null argument");
+    KernelSpec k = parse_kernel(kernel_json);
+    const IntVec prm(params, params + nparams);
+    const std::vector<MemoryMap> mm = maps_of(maps, nmaps);
+    check_maps(k, mm);
+    std::string w;
+    bool hot = false;
+    try {
+      const Recognized R = recognize(k, prm);
+      hot = hot_path_honours(R, k, prm, mm, &w);
+    } catch (const Error& e) {
+      if (e.kind() != ErrorKind::Unsupported) throw;
+      w = e.what();
+    }
+    *hot_path = hot ? 1 : 0;
+    if (why && cap) {
+      std::strncpy(why, w.c_str(), cap - 1);
+      why[cap - 1] = 0;
+    }
+  });
+}
+
+int pcotgpu_create_mapped(const char* kernel_json, const int64_t* params, size_t nparams,
+                          const pcotgpu_map* maps, size_t nmaps, int device, pcotgpu_handle** out) {
+  return guarded([&] {
+    if (!kernel_json || !out || (nmaps && !maps)) fail(ErrorKind::Validation, "null argument");
+    *out = nullptr;
+    KernelSpec k = parse_kernel(kernel_json);
+    std::vector<MemoryMap> mm = maps_of(maps, nmaps);
+    auto h = std::make_unique<pcotgpu_handle>();
+    h->ex = std::make_unique<GpuExecutor>(k, IntVec(params, params + nparams), mm, device);
     *out = h.release();
   });
 }

@@ -27,9 +27,12 @@ struct GAff {
   int64_t c[kMaxIdx];
   int64_t k;
 };
+// One array reference: storage dims (map composed with the subscripts, params
+// folded) with their modulus / extent / stride, and the logical cell id
+// (row-major over the declared extents, the reference's logical_flat).
 struct GRef {
-  int array, rank, aff0, pad;
-  int64_t ext[kMaxRank], stride[kMaxRank];
+  int array, rank, aff0, laff;
+  int64_t ext[kMaxRank], stride[kMaxRank], mod[kMaxRank];
 };
 enum GOpKind { OLit, OAff, ORead, OAdd, OSub, OMul, ODiv, OMin, OMax, ONeg, OSqrt };
 struct GOp {
@@ -48,10 +51,14 @@ struct GDev {
   const GRef* refs;
   const GOp* ops;
   double* const* arr;
-  const int64_t* fbase;  // first flag of each array
-  unsigned* flags;       // dataflow: 1 = cell holds its final value; count pass: writes
+  const int64_t* fbase;  // first flag of each array (logical cells)
+  unsigned* flags;       // dense dataflow: 1 = cell holds its final value; count pass: writes
   unsigned long long* writer;  // count pass: min over writes of (point * nstmt + statement)
   unsigned* bad;               // order pass: 1 if a read precedes (or is) its cell's write
+  const int64_t* sbase;  // first shadow of each array (storage cells)
+  long long* shadow;     // mapped dataflow: logical id held by each storage cell
+  const int64_t* lsize;  // logical cells per array
+  int never_ok;          // dense storage: reads of never-written cells see their initial value
   unsigned long long* next;
   unsigned long long* cnt;  // points, reads, writes
   int* err;                 // 0 ok; s+1: out-of-extent in statement s; -1: wait cap
@@ -69,15 +76,29 @@ PCOT_DEV bool in_domain(const GDev& g, const GStmt& s, const int64_t* z) {
   return true;
 }
 
+// Storage cell (reference phys_flat, exec.cpp:310-325): modulo dims wrap,
+// the others must lie inside the map's extents.
 PCOT_DEV bool cell_of(const GDev& g, const GRef& r, const int64_t* z, int64_t* flat) {
   int64_t f = 0;
   for (int d = 0; d < r.rank; ++d) {
-    const int64_t comp = aff_eval(g.affs[r.aff0 + d], z, g.nidx);
-    if (comp < 0 || comp >= r.ext[d]) return false;
+    int64_t comp = aff_eval(g.affs[r.aff0 + d], z, g.nidx);
+    if (r.mod[d] > 0) {
+      comp %= r.mod[d];
+      if (comp < 0) comp += r.mod[d];
+    } else if (comp < 0 || comp >= r.ext[d]) {
+      return false;
+    }
     f += comp * r.stride[d];
   }
   *flat = f;
   return true;
+}
+
+// Logical cell id (reference logical_flat, exec.cpp:327-331); -1 if outside
+// the declared extents (the run then cannot be checked cell by cell).
+PCOT_DEV int64_t logical_of(const GDev& g, const GRef& r, const int64_t* z) {
+  const int64_t l = aff_eval(g.affs[r.laff], z, g.nidx);
+  return l >= 0 && l < g.lsize[r.array] ? l : -1;
 }
 
 PCOT_DEV void decode(const GDev& g, unsigned long long p, int64_t* z) {
@@ -97,8 +118,20 @@ PCOT_DEV void st_rel_u32(unsigned* p, unsigned v) {
   asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
+PCOT_DEV long long ld_acq_s64(const long long* p) {
+  long long v;
+  asm volatile("ld.acquire.gpu.global.s64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+PCOT_DEV void st_rel_s64(long long* p, long long v) {
+  asm volatile("st.release.gpu.global.s64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
 // Run every statement of point z.  Returns false on an error (recorded).
-template <bool DATAFLOW>
+// DATAFLOW: 0 sequential; 1 dense storage, per-cell ready flags; 2 mapped
+// storage, per-storage-cell shadows holding the logical id of the value they
+// hold (the reference's shadow array, exec.cpp:360-368, used as the wait).
+template <int DATAFLOW>
 PCOT_DEV bool exec_point(const GDev& g, const int64_t* z, unsigned long long* c3) {
   for (int si = 0; si < g.nstmt; ++si) {
     const GStmt s = g.st[si];
@@ -117,7 +150,7 @@ PCOT_DEV bool exec_point(const GDev& g, const int64_t* z, unsigned long long* c3
             atomicCAS(g.err, 0, si + 1);
             return false;
           }
-          if (DATAFLOW) {
+          if (DATAFLOW == 1) {
             const unsigned* fl = g.flags + g.fbase[r.array] + f;
             long long it = 0;
             while (ld_acq_u32(fl) == 0) {
@@ -129,6 +162,29 @@ PCOT_DEV bool exec_point(const GDev& g, const int64_t* z, unsigned long long* c3
               if ((it & 255) == 0 && *reinterpret_cast<volatile int*>(g.err) != 0) return false;
               __nanosleep(64);
             }
+          }
+          if (DATAFLOW == 2) {
+            // wait until the storage cell holds this logical cell's value ...
+            const long long want = logical_of(g, r, z);
+            const long long* sh = g.shadow + g.sbase[r.array] + f;
+            long long it = 0;
+            while (ld_acq_s64(sh) != want) {
+              if (++it > kSpinCapG) {
+                atomicCAS(g.err, 0, -1);
+                return false;
+              }
+              if ((it & 255) == 0 && *reinterpret_cast<volatile int*>(g.err) != 0) return false;
+              __nanosleep(64);
+            }
+            const double v = __ldcg(g.arr[r.array] + f);
+            // ... and still does after the load: a map that is not a universal
+            // occupancy vector could let a later write reuse the cell early
+            if (ld_acq_s64(sh) != want) {
+              atomicCAS(g.err, 0, -2);
+              return false;
+            }
+            stk[sp++] = v;
+            break;
           }
           stk[sp++] = __ldcg(g.arr[r.array] + f);
           break;
@@ -158,7 +214,8 @@ PCOT_DEV bool exec_point(const GDev& g, const int64_t* z, unsigned long long* c3
       return false;
     }
     __stcg(g.arr[w.array] + f, stk[sp - 1]);
-    if (DATAFLOW) st_rel_u32(g.flags + g.fbase[w.array] + f, 1u);
+    if (DATAFLOW == 1) st_rel_u32(g.flags + g.fbase[w.array] + f, 1u);
+    if (DATAFLOW == 2) st_rel_s64(g.shadow + g.sbase[w.array] + f, logical_of(g, w, z));
     c3[0] += 1;
     c3[1] += unsigned(s.nreads);
     c3[2] += 1;
@@ -180,8 +237,13 @@ __global__ void generic_count_kernel(GDev g) {
         atomicCAS(g.err, 0, si + 1);
         continue;
       }
-      atomicAdd(g.flags + g.fbase[w.array] + f, 1u);
-      atomicMin(g.writer + g.fbase[w.array] + f, p * (unsigned long long)g.nstmt + si);
+      const int64_t l = logical_of(g, w, z);
+      if (l < 0) {  // written outside its declared extents: no per-cell check possible
+        atomicOr(g.bad, 1u);
+        continue;
+      }
+      atomicAdd(g.flags + g.fbase[w.array] + l, 1u);
+      atomicMin(g.writer + g.fbase[w.array] + l, p * (unsigned long long)g.nstmt + si);
     }
   }
 }
@@ -206,8 +268,15 @@ __global__ void generic_order_kernel(GDev g) {
         const GRef& r = g.refs[op.arg];
         int64_t f = 0;
         if (!cell_of(g, r, z, &f)) continue;  // reported by the run itself
-        const unsigned long long w = g.writer[g.fbase[r.array] + f];
-        if (w != ~0ull && w >= me) atomicOr(g.bad, 1u);
+        const int64_t l = logical_of(g, r, z);
+        if (l < 0) {
+          atomicOr(g.bad, 1u);
+          continue;
+        }
+        const unsigned long long w = g.writer[g.fbase[r.array] + l];
+        // a never-written cell holds its initial value: fine in dense storage
+        // (ready flag set up front), but in folded storage its slot is shared
+        if (w == ~0ull ? !g.never_ok : w >= me) atomicOr(g.bad, 1u);
       }
     }
   }
@@ -223,8 +292,16 @@ __global__ void generic_flags_kernel(unsigned* flags, int64_t n, unsigned* maxc)
   }
 }
 
+// mapped dataflow: shadows <- inputs hold their own cells (reference
+// init_storage: shadow[f] = f), everything else -1 (nothing written yet)
+__global__ void generic_shadow_init_kernel(long long* sh, int64_t n, int64_t base, int is_input) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
+    sh[base + i] = is_input ? i : -1;
+}
+
 // Persistent dataflow grid: warps take 32 consecutive points in the
-// reference's order; reads wait for their cell's flag.
+// reference's order; reads wait for their cell's flag (dense) or shadow (mapped).
+template <int MODE>
 __global__ void generic_dataflow_kernel(GDev g) {
   const int lane = threadIdx.x & 31;
   unsigned long long c3[3] = {0, 0, 0};
@@ -238,7 +315,7 @@ __global__ void generic_dataflow_kernel(GDev g) {
     const unsigned long long p = base + lane;
     if (ok && p < (unsigned long long)g.npoints) {
       decode(g, p, z);
-      ok = exec_point<true>(g, z, c3);
+      ok = exec_point<MODE>(g, z, c3);
     }
   }
   atomicAdd(&g.cnt[0], c3[0]);
@@ -253,7 +330,7 @@ __global__ void generic_sequential_kernel(GDev g) {
   int64_t z[kMaxIdx];
   for (unsigned long long p = 0; p < (unsigned long long)g.npoints; ++p) {
     decode(g, p, z);
-    if (!exec_point<false>(g, z, c3)) break;
+    if (!exec_point<0>(g, z, c3)) break;
   }
   g.cnt[0] = c3[0];
   g.cnt[1] = c3[1];
@@ -319,8 +396,11 @@ struct GenericPlan {
   std::vector<ArrayKind> kinds;
   std::vector<uint64_t> words;
   std::vector<double*> ptrs;
-  std::vector<int64_t> fbase;
-  int64_t nflags = 0;
+  std::vector<int64_t> fbase;   // logical cells: flags / writer base per array
+  std::vector<int64_t> lsizes;  // logical cells per array (declared extents)
+  std::vector<int64_t> sbase;   // storage cells: shadow base per array
+  int64_t nflags = 0, nshadow = 0;
+  bool mapped = false;          // some map is not the identity at the declared extents
   std::vector<GStmt> st;
   std::vector<GAff> rows, affs;
   std::vector<GRef> refs;
@@ -335,6 +415,9 @@ struct GenericPlan {
   GOp* d_ops = nullptr;
   double** d_arr = nullptr;
   int64_t* d_fbase = nullptr;
+  int64_t* d_sbase = nullptr;
+  int64_t* d_lsize = nullptr;
+  long long* d_shadow = nullptr;
   unsigned* d_flags = nullptr;
   unsigned* d_flags0 = nullptr;  // initial flags (dataflow)
   unsigned long long* d_misc = nullptr;  // next, points, reads, writes
@@ -386,7 +469,8 @@ int64_t eval_extent(const Affine& a, size_t nidx, const IntVec& prm) {
 
 }  // namespace
 
-GenericPlan* generic_plan_create(const KernelSpec& k, const IntVec& prm, int device) {
+GenericPlan* generic_plan_create(const KernelSpec& k, const IntVec& prm,
+                                 const std::vector<MemoryMap>& maps, int device) {
   if (prm.size() != k.params.size()) fail(ErrorKind::DimMismatch, "GpuExecutor: parameter count");
   const size_t full = k.indices.size();
   if (full == 0 || full > size_t(kMaxIdx)) fail(ErrorKind::Unsupported, "generic executor: 1..6 indices");
@@ -394,43 +478,101 @@ GenericPlan* generic_plan_create(const KernelSpec& k, const IntVec& prm, int dev
   P->device = device;
   P->nidx = int(full);
   ckc(cudaSetDevice(device), "cudaSetDevice");
-  // ---- arrays (dense, declaration extents)
+  // ---- arrays: storage by the caller's memory map (reference exec.cpp:
+  // 234-245, MemoryMap::words), else dense at the declared extents
+  auto map_of = [&](const std::string& name) -> const MemoryMap* {
+    for (const auto& m : maps)
+      if (m.array == name) return &m;
+    return nullptr;
+  };
   std::map<std::string, int> aid;
-  int64_t fb = 0;
+  int64_t fb = 0, sb = 0;
   for (const auto& a : k.arrays) {
     if (a.rank > size_t(kMaxRank)) fail(ErrorKind::Unsupported, "generic executor: rank > 6");
-    uint64_t w = 1;
+    uint64_t lw = 1;
+    IntVec decl;
     for (const auto& e : a.extents) {
       const int64_t v = eval_extent(e, full, prm);
       if (v < 0) fail(ErrorKind::Validation, "array " + a.name + ": negative extent");
-      w *= uint64_t(v);
+      lw *= uint64_t(v);
+      decl.push_back(v);
     }
-    if (w > (uint64_t(1) << 33)) fail(ErrorKind::Unsupported, "generic executor: array " + a.name + " too large for dense storage");
+    uint64_t w = lw;
+    if (const MemoryMap* m = map_of(a.name)) {
+      if (m->extents.size() > size_t(kMaxRank)) fail(ErrorKind::Unsupported, "generic executor: storage rank > 6");
+      w = 1;
+      for (int64_t e : m->extents) w *= uint64_t(e);
+      bool identity = m->extents == decl;
+      for (size_t q = 0; identity && q < m->extents.size(); ++q) {
+        identity = m->constant[q] == 0 && m->moduli[q] == 0;
+        for (size_t c = 0; c < a.rank; ++c) identity = identity && m->linear[q][c] == (q == c ? 1 : 0);
+      }
+      if (!identity) P->mapped = true;
+    }
+    if (w > (uint64_t(1) << 33)) fail(ErrorKind::Unsupported, "generic executor: array " + a.name + " storage too large");
     aid[a.name] = int(P->names.size());
     P->names.push_back(a.name);
     P->kinds.push_back(a.kind);
     P->words.push_back(w);
     P->fbase.push_back(fb);
-    fb += int64_t(w);
+    P->lsizes.push_back(int64_t(lw));
+    P->sbase.push_back(sb);
+    fb += int64_t(lw);
+    sb += int64_t(w);
     double* d = nullptr;
     ckc(cudaMalloc(&d, std::max<uint64_t>(w, 1) * 8), "cudaMalloc");
     P->ptrs.push_back(d);
   }
   P->nflags = fb;
+  P->nshadow = sb;
   auto make_ref = [&](const std::string& arr, const std::vector<Affine>& subs, size_t depth) {
     const ArrayDecl* ad = k.find_array(arr);
+    if (subs.size() != ad->rank) fail(ErrorKind::Validation, "Executor: subscript arity for " + arr);
     GRef r;
     std::memset(&r, 0, sizeof(r));
     r.array = aid.at(arr);
-    r.rank = int(ad->rank);
+    std::vector<GAff> cell;
+    for (const auto& s : subs) cell.push_back(fold(s, depth, full, prm));
+    // logical id over the declared extents
+    GAff l;
+    std::memset(&l, 0, sizeof(l));
+    int64_t lstride = 1;
+    for (int d = int(ad->rank) - 1; d >= 0; --d) {
+      for (size_t t = 0; t < full; ++t) l.c[t] += lstride * cell[size_t(d)].c[t];
+      l.k += lstride * cell[size_t(d)].k;
+      lstride *= eval_extent(ad->extents[size_t(d)], full, prm);
+    }
+    r.laff = int(P->affs.size());
+    P->affs.push_back(l);
     r.aff0 = int(P->affs.size());
+    const MemoryMap* m = map_of(arr);
+    if (m) {  // storage_k = map_k(cell): compose (reference build_ref, exec.cpp:150-163)
+      r.rank = int(m->extents.size());
+      for (int q = 0; q < r.rank; ++q) {
+        GAff a;
+        std::memset(&a, 0, sizeof(a));
+        a.k = m->constant[size_t(q)];
+        for (size_t j = 0; j < ad->rank; ++j) {
+          const int64_t wgt = m->linear[size_t(q)][j];
+          a.k += wgt * cell[j].k;
+          for (size_t t = 0; t < full; ++t) a.c[t] += wgt * cell[j].c[t];
+        }
+        P->affs.push_back(a);
+        r.ext[q] = m->extents[size_t(q)];
+        r.mod[q] = m->moduli[size_t(q)];
+      }
+    } else {
+      r.rank = int(ad->rank);
+      for (int q = 0; q < r.rank; ++q) {
+        P->affs.push_back(cell[size_t(q)]);
+        r.ext[q] = eval_extent(ad->extents[size_t(q)], full, prm);
+      }
+    }
     int64_t stride = 1;
     for (int d = r.rank - 1; d >= 0; --d) {
-      r.ext[d] = eval_extent(ad->extents[size_t(d)], full, prm);
       r.stride[d] = stride;
       stride *= r.ext[d];
     }
-    for (const auto& s : subs) P->affs.push_back(fold(s, depth, full, prm));
     P->refs.push_back(r);
     return int(P->refs.size() - 1);
   };
@@ -540,6 +682,10 @@ GenericPlan* generic_plan_create(const KernelSpec& k, const IntVec& prm, int dev
   P->d_ops = upload(P->ops);
   P->d_arr = upload(P->ptrs);
   P->d_fbase = upload(P->fbase);
+  P->d_sbase = upload(P->sbase);
+  P->d_lsize = upload(P->lsizes);
+  if (P->mapped)
+    ckc(cudaMalloc(&P->d_shadow, std::max<int64_t>(P->nshadow, 1) * sizeof(long long)), "cudaMalloc");
   ckc(cudaMalloc(&P->d_flags, std::max<int64_t>(P->nflags, 1) * sizeof(unsigned)), "cudaMalloc");
   ckc(cudaMalloc(&P->d_flags0, std::max<int64_t>(P->nflags, 1) * sizeof(unsigned)), "cudaMalloc");
   ckc(cudaMalloc(&P->d_misc, 4 * sizeof(unsigned long long)), "cudaMalloc");
@@ -558,6 +704,9 @@ void generic_plan_destroy(GenericPlan* p) {
   cudaFree(p->d_ops);
   cudaFree(p->d_arr);
   cudaFree(p->d_fbase);
+  cudaFree(p->d_sbase);
+  cudaFree(p->d_lsize);
+  cudaFree(p->d_shadow);
   cudaFree(p->d_flags);
   cudaFree(p->d_flags0);
   cudaFree(p->d_misc);
@@ -599,6 +748,10 @@ static GDev dev_args(GenericPlan* p) {
   g.ops = p->d_ops;
   g.arr = p->d_arr;
   g.fbase = p->d_fbase;
+  g.sbase = p->d_sbase;
+  g.lsize = p->d_lsize;
+  g.shadow = p->d_shadow;
+  g.never_ok = p->mapped ? 0 : 1;
   g.flags = p->d_flags;
   g.next = p->d_misc;
   g.cnt = p->d_misc + 1;
@@ -617,6 +770,12 @@ cudaError_t generic_run(GenericPlan* p, cudaStream_t s, GenericCounts* counts, s
       if ((e = cudaMemsetAsync(p->ptrs[i], 0, p->words[i] * 8, s)) != cudaSuccess) return e;
   if ((e = cudaMemsetAsync(p->d_err, 0, sizeof(int), s)) != cudaSuccess) return e;
   if ((e = cudaMemsetAsync(p->d_misc, 0, 4 * sizeof(unsigned long long), s)) != cudaSuccess) return e;
+  // the per-cell checks index the logical cells (flags 4 B + writer 8 B each)
+  const bool checkable = p->nflags <= (int64_t(1) << 31);
+  if (!p->counted && !checkable) {
+    p->dataflow = false;  // too large to verify: the reference's sequential order
+    p->counted = true;
+  }
   if (!p->counted) {  // write counts once per plan: single assignment -> dataflow grid
     if ((e = cudaMemsetAsync(p->d_flags, 0, std::max<int64_t>(p->nflags, 1) * sizeof(unsigned), s)) != cudaSuccess)
       return e;
@@ -652,14 +811,24 @@ cudaError_t generic_run(GenericPlan* p, cudaStream_t s, GenericCounts* counts, s
                              cudaMemcpyDeviceToDevice, s)) != cudaSuccess)
       return e;
     p->counted = true;
-  } else if (p->dataflow) {
+  } else if (p->dataflow && !p->mapped) {
     if ((e = cudaMemcpyAsync(p->d_flags, p->d_flags0, std::max<int64_t>(p->nflags, 1) * sizeof(unsigned),
                              cudaMemcpyDeviceToDevice, s)) != cudaSuccess)
       return e;
   }
+  if (p->dataflow && p->mapped) {  // storage reset: shadows say what each cell holds
+    for (size_t i = 0; i < p->names.size(); ++i) {
+      if (!p->words[i]) continue;
+      generic_shadow_init_kernel<<<sms * 2, 256, 0, s>>>(p->d_shadow, int64_t(p->words[i]), p->sbase[i],
+                                                         p->kinds[i] == ArrayKind::Input ? 1 : 0);
+      count_launch();
+    }
+  }
   if (p->npoints > 0) {
-    if (p->dataflow) {
-      generic_dataflow_kernel<<<sms * 4, 128, 0, s>>>(g);
+    if (p->dataflow && p->mapped) {
+      generic_dataflow_kernel<2><<<sms * 4, 128, 0, s>>>(g);
+    } else if (p->dataflow) {
+      generic_dataflow_kernel<1><<<sms * 4, 128, 0, s>>>(g);
     } else {
       generic_sequential_kernel<<<1, 32, 0, s>>>(g);
     }
@@ -673,7 +842,9 @@ cudaError_t generic_run(GenericPlan* p, cudaStream_t s, GenericCounts* counts, s
   if (err != 0) {
     if (err_msg)
       *err_msg = err > 0 ? "out-of-extent access in statement " + p->stmt_ids[size_t(err - 1)]
-                         : std::string("dataflow wait exceeded its bound (kernel not legal in lexicographic order)");
+                 : err == -2 ? std::string("dependence violation: a storage cell was reused before its "
+                                           "value was read (the memory map is not a universal occupancy vector)")
+                             : std::string("dataflow wait exceeded its bound (kernel not legal in lexicographic order)");
     return cudaErrorInvalidValue;
   }
   if (counts) {

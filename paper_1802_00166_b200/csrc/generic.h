@@ -4,15 +4,22 @@
 // the remaining corpus kernels — triangle, lud, osp, heat1d-fig7 — run on the
 // device instead of being rejected).
 //
-// Storage: every array dense at its declared extents (the reference's
-// single-assignment layout, exec.cpp:234-245 without memory maps).
+// Storage: laid out by the caller's memory maps (reference exec.cpp:142-185,
+// 234-245: words = product of the map extents, storage_k = map_k(cell) mod
+// moduli_k, out-of-extent checks on the unfolded dims), or dense at the
+// declared extents when no maps are given (single-assignment layout).
 // Schedule:
-//   * single-assignment kernels (every cell written at most once — checked on
-//     the device by a write-count pass): a persistent grid takes points in the
-//     reference's lexicographic order from an atomic counter; every read waits
-//     for its cell's ready flag (acquire), every write publishes it (release).
-//     A read only ever waits on a point earlier in that order, which is
-//     already running or done, so the grid cannot deadlock;
+//   * single-assignment kernels (every logical cell written at most once, and
+//     every write before its reads in the reference's order — both checked on
+//     the device by a counting pass over the logical cells): a persistent grid
+//     takes points in the reference's lexicographic order from an atomic
+//     counter; every read waits for its cell (dense storage: a ready flag;
+//     folded storage: the storage cell's shadow = logical id of the value it
+//     holds, the reference's shadow array), every write publishes it.  A read
+//     only ever waits on a point earlier in that order, which is already
+//     running or done, so the grid cannot deadlock; folded storage is safe
+//     because allocate()'s maps fold along universal occupancy vectors (any
+//     dependence-respecting order), and a reused cell is detected, not read;
 //   * otherwise (cells overwritten, e.g. osp's C): one device thread walks the
 //     points in the reference's order.
 // Per point, the statements whose domains contain it run in declaration
@@ -36,7 +43,11 @@ struct GenericPlan;
 // extents, projects every statement domain onto each index (Fourier-Motzkin)
 // for the point box, compiles bodies to postfix programs.  Throws Unbounded /
 // Validation like the reference.
-GenericPlan* generic_plan_create(const KernelSpec& k, const IntVec& params, int device);
+// `maps` (may be empty): the reference's MemoryMaps — storage of each mapped
+// array is laid out exactly by its map (words, modulo folding, extents), as the
+// reference's ArrayStore is; unmapped arrays are dense at declared extents.
+GenericPlan* generic_plan_create(const KernelSpec& k, const IntVec& params,
+                                 const std::vector<MemoryMap>& maps, int device);
 void generic_plan_destroy(GenericPlan* p);
 
 // Array access (dense, declaration extents).

@@ -778,6 +778,8 @@ Recognized recognize_stencil(const KernelSpec& k, const IntVec& prm) {
     sk.b[r + 1] = u.k;
   }
   sk.Ainv = inverse_unimodular(sk.A);
+  R.Ainv = sk.Ainv;
+  R.b = sk.b;
   R.T = prm[tparam];
   // ---- classify temp-writing statements
   std::string update_canon;
@@ -1004,10 +1006,146 @@ Recognized recognize_gemm(const KernelSpec& k, const IntVec& prm) {
   }
   R.N = n;
   R.inputs = {ins[0]->name, ins[1]->name};
+  R.Ainv.assign(nidx, IntVec(nidx, 0));
+  for (size_t i = 0; i < nidx; ++i) R.Ainv[i][i] = 1;
+  R.b.assign(nidx, 0);
   return R;
 }
 
+
+int64_t eval_param_affine(const Affine& a, size_t nidx, const IntVec& prm) {
+  int64_t v = a.k;
+  const size_t off = a.c.size() >= nidx + prm.size() ? nidx : 0;
+  for (size_t j = 0; j < prm.size(); ++j)
+    if (off + j < a.c.size()) v += a.c[off + j] * prm[j];
+  return v;
+}
+
 }  // namespace
+
+void check_maps(const KernelSpec& k, const std::vector<MemoryMap>& maps) {
+  for (const auto& m : maps) {
+    const ArrayDecl* a = k.find_array(m.array);
+    if (!a) fail(ErrorKind::Validation, "Executor: memory map for unknown array " + m.array);
+    const size_t pd = m.extents.size();
+    if (m.linear.size() != pd || m.constant.size() != pd || m.moduli.size() != pd)
+      fail(ErrorKind::DimMismatch, "Executor: malformed memory map for " + m.array);
+    for (const auto& row : m.linear)
+      if (row.size() != a->rank) fail(ErrorKind::DimMismatch, "Executor: memory map arity for " + m.array);
+    for (size_t q = 0; q < pd; ++q)
+      if (m.extents[q] < 0 || m.moduli[q] < 0)
+        fail(ErrorKind::Validation, "Executor: negative extent or modulus in the map of " + m.array);
+  }
+  for (const auto& a : k.arrays) {
+    int n = 0;
+    for (const auto& m : maps) n += m.array == a.name;
+    if (n == 0) fail(ErrorKind::Validation, "Executor: no memory map for array " + a.name);
+  }
+}
+
+bool hot_path_honours(const Recognized& R, const KernelSpec& k, const IntVec& prm,
+                      const std::vector<MemoryMap>& maps, std::string* why) {
+  const size_t nidx = k.indices.size();
+  auto no = [&](const std::string& m) {
+    if (why) *why = m;
+    return false;
+  };
+  // occupancy vector of the temp, in its cell coordinates (= kernel indices)
+  IntVec u0(nidx, 0);
+  switch (R.family) {
+    case Family::Stencil2D5:
+    case Family::Stencil3D7: u0.assign(nidx, 2); break;        // (t mod 2, x - t, ...)
+    case Family::GaussSeidel2D9: u0 = {1, 1, 2}; break;        // (t mod 1, x - t, y - 2t)
+    case Family::Gemm: u0 = {0, 0, 1}; break;                  // (i, j, k mod 1)
+    default: return no("not a hot-path kernel");
+  }
+  for (const auto& a : k.arrays) {
+    const MemoryMap* m = nullptr;
+    for (const auto& mm : maps)
+      if (mm.array == a.name) m = &mm;
+    if (!m) return no("no map for " + a.name);
+    const size_t r = a.rank, pd = m->extents.size();
+    bool identity = pd == r;
+    for (size_t q = 0; identity && q < pd; ++q) {
+      identity = m->constant[q] == 0 && m->moduli[q] == 0;
+      for (size_t c = 0; c < r; ++c) identity = identity && m->linear[q][c] == (q == c ? 1 : 0);
+    }
+    IntVec decl(r);
+    for (size_t q = 0; q < r; ++q) decl[q] = eval_param_affine(a.extents[q], nidx, prm);
+    if (a.kind != ArrayKind::Temp) {
+      if (!identity || m->extents != decl)
+        return no("the " + a.name + " map is not the identity at the declared extents");
+      continue;
+    }
+    if (identity) {  // single assignment: every cell the run touches lies in the declared box
+      for (size_t q = 0; q < r; ++q)
+        if (m->extents[q] < decl[q]) return no("the " + a.name + " map is smaller than its declared extents");
+      continue;
+    }
+    // folded along u = c * (e_j0 - sum_i alpha_i e_i): linear = I except column j0
+    if (pd != r) return no("the " + a.name + " map changes the rank");
+    int j0 = -1;
+    for (size_t q = 0; q < pd; ++q)
+      if (m->moduli[q] > 0) {
+        if (j0 >= 0) return no("the " + a.name + " map folds more than one dimension");
+        j0 = int(q);
+      }
+    if (j0 < 0) return no("the " + a.name + " map is neither single-assignment nor folded");
+    const int64_t c = m->moduli[size_t(j0)];
+    IntVec u(r, 0);
+    u[size_t(j0)] = c;
+    for (size_t q = 0; q < pd; ++q)
+      for (size_t cc = 0; cc < r; ++cc) {
+        const int64_t v = m->linear[q][cc];
+        if (cc == size_t(j0) && q != size_t(j0)) {
+          u[q] = -v * c;
+        } else if (v != (q == cc ? 1 : 0)) {
+          return no("the " + a.name + " map is not an occupancy-vector fold");
+        }
+      }
+    // u must be a positive multiple of the kernel's occupancy vector
+    int64_t mult = 0;
+    for (size_t q = 0; q < r; ++q)
+      if (u0[q]) {
+        if (u[q] % u0[q]) return no("the " + a.name + " map folds along a vector the kernel does not allow");
+        mult = u[q] / u0[q];
+        break;
+      }
+    if (mult < 1) return no("the " + a.name + " map folds along a vector the kernel does not allow");
+    for (size_t q = 0; q < r; ++q)
+      if (u[q] != mult * u0[q]) return no("the " + a.name + " map folds along a vector the kernel does not allow");
+    // extents: every cell the temp-writing statements touch must map inside
+    // (the modulo dimension needs extent >= modulus)
+    if (m->extents[size_t(j0)] < c)
+      fail(ErrorKind::Validation, "out-of-extent storage for " + a.name + ": folded extent below its modulus");
+    IntVec lo(pd, INT64_MAX), hi(pd, INT64_MIN);
+    for (const auto& b : R.stmts) {
+      if (b.role == "final" || b.lo.empty()) continue;
+      bool empty = false;
+      for (size_t q = 0; q < b.lo.size(); ++q) empty = empty || b.lo[q] > b.hi[q];
+      if (empty) continue;
+      const size_t nb = b.lo.size();
+      for (uint64_t corner = 0; corner < (uint64_t(1) << nb); ++corner) {
+        IntVec uu(nb), z(nidx, 0);
+        for (size_t q = 0; q < nb; ++q) uu[q] = (corner >> q & 1) ? b.hi[q] : b.lo[q];
+        for (size_t i = 0; i < nidx; ++i)
+          for (size_t j = 0; j < nidx && j < nb; ++j) z[i] += R.Ainv[i][j] * (uu[j] - R.b[j]);
+        for (size_t q = 0; q < pd; ++q) {
+          int64_t v = m->constant[q];
+          for (size_t cc = 0; cc < r; ++cc) v += m->linear[q][cc] * z[cc];
+          lo[q] = std::min(lo[q], v);
+          hi[q] = std::max(hi[q], v);
+        }
+      }
+    }
+    for (size_t q = 0; q < pd; ++q)
+      if (q != size_t(j0) && lo[q] <= hi[q] && (lo[q] < 0 || hi[q] >= m->extents[q]))
+        fail(ErrorKind::Validation, "out-of-extent access to " + a.name + " dim " + std::to_string(q) +
+                                        " under its memory map (storage range [" + std::to_string(lo[q]) +
+                                        ", " + std::to_string(hi[q]) + "])");
+  }
+  return true;
+}
 
 Recognized recognize(const KernelSpec& k, const IntVec& params) {
   if (params.size() != k.params.size()) fail(ErrorKind::DimMismatch, "GpuExecutor: parameter count");

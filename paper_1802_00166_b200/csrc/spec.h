@@ -100,6 +100,21 @@ struct StmtBox {
   uint64_t reads_per_point = 0;
 };
 
+// Storage map of one array (reference memalloc.hpp:14-33):
+//   storage_k = (linear[k] . cell + constant[k]) mod moduli[k]  (moduli 0: none),
+// in [0, extents[k]); storage is row-major over `extents`.
+struct MemoryMap {
+  std::string array;
+  std::vector<IntVec> linear;  // storage rank x array rank
+  IntVec constant, moduli, extents;
+  bool single_assignment = false;
+  int64_t words() const {
+    int64_t w = 1;
+    for (int64_t e : extents) w *= e;
+    return w;
+  }
+};
+
 // What the recognizer established about a kernel at a parameter binding.
 struct Recognized {
   Family family = Family::Stencil2D5;
@@ -111,9 +126,25 @@ struct Recognized {
   std::string temp, output;
   std::vector<StmtBox> stmts;
   uint64_t points = 0, reads = 0, writes = 0;  // closed-form ExecResult counters
+  // kernel index z of un-skewed point u (box coordinates): z = Ainv (u - b)
+  std::vector<IntVec> Ainv;
+  IntVec b;
 };
 
 Recognized recognize(const KernelSpec& k, const IntVec& params);
+
+// The structural checks the reference makes when it builds storage from maps
+// (exec.cpp:134-141 map_of, 142-185 build_ref): one map per array, arities.
+void check_maps(const KernelSpec& k, const std::vector<MemoryMap>& maps);
+// True if a recognized kernel's device layout reproduces the reference's
+// results under `maps`: inputs/outputs stored as the identity at their
+// declared extents, the temp either single-assignment or folded along a
+// positive multiple of the kernel's occupancy vector (the allocate() maps,
+// memalloc.cpp:542-595).  Storage extents that cannot hold the cells the run
+// touches raise Validation, as the reference's out-of-extent check does
+// (exec.cpp:318-323).  `why` says what did not match.
+bool hot_path_honours(const Recognized& R, const KernelSpec& k, const IntVec& prm,
+                      const std::vector<MemoryMap>& maps, std::string* why);
 const char* family_name(Family f);
 
 uint64_t fnv1a(const void* data, size_t n, uint64_t h = 0xcbf29ce484222325ULL);

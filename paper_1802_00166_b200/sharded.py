@@ -14,8 +14,10 @@ The reference has no distributed path; results must equal the
 single-grid run bit for bit, which the per-point arithmetic guarantees as
 long as the ghost rows hold the neighbour's step-t0 values.
 
-The slab kernel is injected (`advance`) so the same exchange logic runs with
-the sm_100a kernel on GPUs and is tested with gloo on CPU.
+The slab kernel is injected (`advance`) so the same exchange logic — the
+same edge-strips-first / post sends / interior / wait sequence, line for
+line — runs with the sm_100a kernel on GPUs and with a CPU restatement under
+gloo in the tests; on CPU the "streams" are no-op lanes.
 
 halo="p2p" fuses the exchange into the stencil kernel instead: both slabs
 live in symmetric memory (torch.distributed._symmetric_memory, peer buffers
@@ -23,8 +25,11 @@ mapped over NVLink), one launch per block advances every owned row and
 stores its first/last bt output rows a second time, straight into the
 neighbours' ghost rows (`pcotgpu_s2d5_advance_p2p`); a device-side barrier on
 the stream then orders the block against the neighbours' next one.  No
-send/recv, no separate edge launches.
+send/recv, no separate edge launches.  The fused kernel and the barrier are
+injectable too (`advance_p2p`, `barrier`, `buffers`), so the ordering logic
+runs on CPU with the mirror stores emulated into shared-memory buffers.
 """
+import contextlib
 import ctypes
 
 import torch
@@ -33,13 +38,14 @@ import torch.distributed as dist
 import paper_1802_00166_b200 as P
 
 
-def mirror_targets(peer_out_origin_up, peer_out_origin_dn, rows, ld):
-    """Byte addresses the P2P kernel takes as mirror_up / mirror_dn: output row r
-    of this slab lands at mirror + (r*ld + col)*8, i.e. the upper neighbour's
+def mirror_targets(peer_out_origin_up, peer_out_origin_dn, rows, ld, elem=8):
+    """Addresses the P2P kernel takes as mirror_up / mirror_dn: output row r of
+    this slab lands at mirror + (r*ld + col)*elem, i.e. the upper neighbour's
     row R + r (its ghost rows below, r < bt) and the lower neighbour's row r - R
-    (its ghost rows above, r >= R - bt).  None = no neighbour on that side."""
-    up = None if peer_out_origin_up is None else peer_out_origin_up + rows * ld * 8
-    dn = None if peer_out_origin_dn is None else peer_out_origin_dn - rows * ld * 8
+    (its ghost rows above, r >= R - bt).  None = no neighbour on that side.
+    elem=8: byte addresses (the kernel); elem=1: element offsets (emulation)."""
+    up = None if peer_out_origin_up is None else peer_out_origin_up + rows * ld * elem
+    dn = None if peer_out_origin_dn is None else peer_out_origin_dn - rows * ld * elem
     return up, dn
 
 
@@ -55,7 +61,8 @@ class ShardedStencil2D:
     global grid's edges (ring_hold=0: literal 0.0, 1: copied forward)."""
 
     def __init__(self, rows_per_rank, cols, T, bt, ring_hold=0, order=0, device=None,
-                 advance=None, geometry=None, group=None, halo="nccl"):
+                 advance=None, geometry=None, group=None, halo="nccl", advance_p2p=None,
+                 barrier=None, buffers=None):
         self.rank = dist.get_rank() if dist.is_initialized() else 0
         self.world = dist.get_world_size() if dist.is_initialized() else 1
         self.group = group
@@ -77,9 +84,12 @@ class ShardedStencil2D:
         # (at world size 1 the symmetric-memory path still runs: no neighbours,
         # so no mirror stores, but the allocation, rendezvous and barrier do)
         self.p2p = halo == "p2p"
-        if self.p2p and not (self.on_gpu and dist.is_initialized()):
+        emulated = advance_p2p is not None and barrier is not None and buffers is not None
+        if self.p2p and not emulated and not (self.on_gpu and dist.is_initialized()):
             raise ValueError("halo='p2p' needs CUDA devices and an initialised process group")
-        if self.p2p:
+        if buffers is not None:  # caller-owned slabs (the P2P emulation's shared memory)
+            self.buf = list(buffers)
+        elif self.p2p:
             from torch.distributed import _symmetric_memory as symm
 
             grp = self.group if self.group is not None else dist.group.WORLD
@@ -93,6 +103,8 @@ class ShardedStencil2D:
             self.buf = [torch.zeros(total, dtype=torch.float64, device=self.device) for _ in range(2)]
         self.cur = 0
         self.advance = advance or self._advance_cuda
+        self.advance_p2p = advance_p2p or self._advance_p2p
+        self.barrier = barrier or (lambda b: self.symm[b].barrier(channel=0))
         if self.on_gpu:
             self.s_edge = torch.cuda.Stream(device=self.device, priority=-1)
             self.s_inner = torch.cuda.Stream(device=self.device)
@@ -197,41 +209,57 @@ class ShardedStencil2D:
         else:
             fn()
 
+    # lanes: CUDA streams on the GPU; on CPU the same sequence with no-op lanes
+    def _main(self):
+        return torch.cuda.current_stream(self.device) if self.on_gpu else None
+
+    def _on(self, lane):
+        return torch.cuda.stream(lane) if lane is not None else contextlib.nullcontext()
+
+    def _fork(self):
+        if not self.on_gpu:
+            return None, None
+        main = self._main()
+        self.s_edge.wait_stream(main)
+        self.s_inner.wait_stream(main)
+        return self.s_edge, self.s_inner
+
+    def _join(self):
+        if self.on_gpu:
+            main = self._main()
+            main.wait_stream(self.s_edge)
+            main.wait_stream(self.s_inner)
+
     def block(self, bt, record=False):
         """Advance all owned rows by bt steps, exchanging boundary rows."""
         src, dst = self.cur, self.cur ^ 1
         if self.world == 1 and not self.p2p:
-            stream = torch.cuda.current_stream(self.device) if self.on_gpu else None
-            self._timed(lambda: self.advance(src, dst, 0, self.R, bt, stream), stream, record)
-        elif not self.on_gpu:
-            self.advance(src, dst, 0, self.R, bt, None)
-            self.exchange_sync(dst, bt)
+            main = self._main()
+            self._timed(lambda: self.advance(src, dst, 0, self.R, bt, main), main, record)
         elif self.p2p:
             # one launch: owned rows + their mirror stores into the neighbours'
             # ghost rows of `dst`; the barrier (after this kernel, on the same
             # stream) waits for the neighbours' kernels of this block, whose
             # stores filled our ghost rows, before anyone starts the next block
-            main = torch.cuda.current_stream(self.device)
-            self._timed(lambda: self._advance_p2p(src, dst, bt, main), main, record)
-            self.symm[dst].barrier(channel=0)
+            main = self._main()
+            self._timed(lambda: self.advance_p2p(src, dst, bt, main), main, record)
+            self.barrier(dst)
         else:
-            main = torch.cuda.current_stream(self.device)
-            self.s_edge.wait_stream(main)
-            self.s_inner.wait_stream(main)
+            # overlapped NCCL exchange: boundary strips first, their rows go out
+            # while the interior is advanced on the other lane; the receives
+            # complete before the next block reads the ghost rows
+            edge, inner = self._fork()
             e = self.bt if self.R >= 2 * self.bt else self.R
-            with torch.cuda.stream(self.s_edge):
-                self._timed(lambda: self.advance(src, dst, 0, e, bt, self.s_edge), self.s_edge, record)
-                self._timed(lambda: self.advance(src, dst, self.R - e, self.R, bt, self.s_edge),
-                            self.s_edge, record)
+            with self._on(edge):
+                self._timed(lambda: self.advance(src, dst, 0, e, bt, edge), edge, record)
+                self._timed(lambda: self.advance(src, dst, self.R - e, self.R, bt, edge), edge, record)
                 reqs = dist.batch_isend_irecv(self._ops(dst, bt))
-            with torch.cuda.stream(self.s_inner):
-                self._timed(lambda: self.advance(src, dst, e, self.R - e, bt, self.s_inner),
-                            self.s_inner, record)
-            with torch.cuda.stream(self.s_edge):
+            with self._on(inner):
+                self._timed(lambda: self.advance(src, dst, e, self.R - e, bt, inner), inner, record)
+            with self._on(edge):
                 for r in reqs:
                     r.wait()
-            main.wait_stream(self.s_edge)
-            main.wait_stream(self.s_inner)
+            self._join()
         self.cur = dst
 
     def run(self, record=False):
