@@ -71,7 +71,9 @@ typedef struct {
 typedef struct {
   uint64_t points, reads, writes;
   int32_t violation; /* always 0: legality holds by construction */
-  int32_t bt;        /* temporal block depth actually used */
+  int32_t bt;        /* temporal block depth actually used; device interpreter
+                        (family 5): 0 sequential, 1 dataflow grid over ready
+                        flags, 2 dataflow grid over storage shadows (maps) */
   uint64_t checksum; /* FNV-1a over output bytes (formats.md CHECKSUM) */
   double device_ms;  /* CUDA-event time of the device work */
   uint64_t launches; /* kernels launched by this run */

@@ -94,6 +94,8 @@ class GpuExecutor {
     check(pcotgpu_array_base(h_, a.c_str(), &b));
     return b;
   }
+  // pcotgpu_result.bt of the last run (temporal depth; interpreter schedule)
+  int last_bt() const { return last_bt_; }
   int family() const {
     pcotgpu_kernel_info i{};
     check(pcotgpu_info(h_, &i));
@@ -112,6 +114,7 @@ class GpuExecutor {
     pcotgpu_result r{};
     check(pcotgpu_run(h_, s, &r));
     cache_.clear();
+    last_bt_ = r.bt;
     ExecResult e;
     e.points = r.points;
     e.reads = r.reads;
@@ -121,6 +124,7 @@ class GpuExecutor {
     return e;
   }
   pcotgpu_handle* h_ = nullptr;
+  int last_bt_ = 0;
   mutable std::map<std::string, std::vector<double>> cache_;
 };
 

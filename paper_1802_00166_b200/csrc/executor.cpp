@@ -339,7 +339,7 @@ struct GpuExecutor::Impl {
       case Family::Stencil3D7: r.bt = run_stencil3d(o); break;
       case Family::GaussSeidel2D9: r.bt = run_gs(o); break;
       case Family::Gemm: r.bt = run_gemm(o); break;
-      case Family::Generic: run_generic(); break;
+      case Family::Generic: run_generic(); r.bt = gcounts.mode; break;  // interpreter schedule
     }
     ck(cudaEventRecord(ev1, stream), "cudaEventRecord");
     ck(cudaEventSynchronize(ev1), "run");

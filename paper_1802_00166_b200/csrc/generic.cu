@@ -5,6 +5,7 @@
 // body is the postfix program of the reference's flatten (exec.cpp:187-224).
 #include <algorithm>
 #include <climits>
+#include <cstdio>
 #include <cmath>
 #include <cstring>
 #include <functional>
@@ -59,6 +60,7 @@ struct GDev {
   long long* shadow;     // mapped dataflow: logical id held by each storage cell
   const int64_t* lsize;  // logical cells per array
   int never_ok;          // dense storage: reads of never-written cells see their initial value
+  const int* is_input;   // per array
   unsigned long long* next;
   unsigned long long* cnt;  // points, reads, writes
   int* err;                 // 0 ok; s+1: out-of-extent in statement s; -1: wait cap
@@ -126,6 +128,17 @@ PCOT_DEV long long ld_acq_s64(const long long* p) {
 PCOT_DEV void st_rel_s64(long long* p, long long v) {
   asm volatile("st.release.gpu.global.s64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
+PCOT_DEV void st_rlx_s64(long long* p, long long v) {
+  asm volatile("st.relaxed.gpu.global.s64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+PCOT_DEV double ld_acq_f64(const double* p) {
+  double v;
+  asm volatile("ld.acquire.gpu.global.f64 %0, [%1];" : "=d"(v) : "l"(p) : "memory");
+  return v;
+}
+PCOT_DEV void st_rel_f64(double* p, double v) {
+  asm volatile("st.release.gpu.global.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
+}
 
 // Run every statement of point z.  Returns false on an error (recorded).
 // DATAFLOW: 0 sequential; 1 dense storage, per-cell ready flags; 2 mapped
@@ -176,7 +189,9 @@ PCOT_DEV bool exec_point(const GDev& g, const int64_t* z, unsigned long long* c3
               if ((it & 255) == 0 && *reinterpret_cast<volatile int*>(g.err) != 0) return false;
               __nanosleep(64);
             }
-            const double v = __ldcg(g.arr[r.array] + f);
+            // (seqlock: a writer invalidates the shadow before its data store,
+            // so a load that saw new data also sees the changed shadow)
+            const double v = ld_acq_f64(g.arr[r.array] + f);
             // ... and still does after the load: a map that is not a universal
             // occupancy vector could let a later write reuse the cell early
             if (ld_acq_s64(sh) != want) {
@@ -213,9 +228,15 @@ PCOT_DEV bool exec_point(const GDev& g, const int64_t* z, unsigned long long* c3
       atomicCAS(g.err, 0, si + 1);
       return false;
     }
-    __stcg(g.arr[w.array] + f, stk[sp - 1]);
+    if (DATAFLOW == 2) {  // invalidate, data, publish (see the reader's seqlock)
+      long long* sh = g.shadow + g.sbase[w.array] + f;
+      st_rlx_s64(sh, -2);
+      st_rel_f64(g.arr[w.array] + f, stk[sp - 1]);
+      st_rel_s64(sh, logical_of(g, w, z));
+    } else {
+      __stcg(g.arr[w.array] + f, stk[sp - 1]);
+    }
     if (DATAFLOW == 1) st_rel_u32(g.flags + g.fbase[w.array] + f, 1u);
-    if (DATAFLOW == 2) st_rel_s64(g.shadow + g.sbase[w.array] + f, logical_of(g, w, z));
     c3[0] += 1;
     c3[1] += unsigned(s.nreads);
     c3[2] += 1;
@@ -239,7 +260,7 @@ __global__ void generic_count_kernel(GDev g) {
       }
       const int64_t l = logical_of(g, w, z);
       if (l < 0) {  // written outside its declared extents: no per-cell check possible
-        atomicOr(g.bad, 1u);
+        atomicOr(g.bad, 4u);
         continue;
       }
       atomicAdd(g.flags + g.fbase[w.array] + l, 1u);
@@ -270,13 +291,18 @@ __global__ void generic_order_kernel(GDev g) {
         if (!cell_of(g, r, z, &f)) continue;  // reported by the run itself
         const int64_t l = logical_of(g, r, z);
         if (l < 0) {
-          atomicOr(g.bad, 1u);
+          atomicOr(g.bad, 8u);
           continue;
         }
         const unsigned long long w = g.writer[g.fbase[r.array] + l];
         // a never-written cell holds its initial value: fine in dense storage
-        // (ready flag set up front), but in folded storage its slot is shared
-        if (w == ~0ull ? !g.never_ok : w >= me) atomicOr(g.bad, 1u);
+        // (ready flag set up front) and for inputs (their shadows hold their
+        // own ids), but a folded temp's slot is shared
+        if (w == ~0ull) {
+          if (!g.never_ok && !g.is_input[r.array]) atomicOr(g.bad, 2u);
+        } else if (w >= me) {
+          atomicOr(g.bad, 1u);
+        }
       }
     }
   }
@@ -328,9 +354,14 @@ __global__ void generic_sequential_kernel(GDev g) {
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
   unsigned long long c3[3] = {0, 0, 0};
   int64_t z[kMaxIdx];
+  if (g.npoints > 0) decode(g, 0, z);
   for (unsigned long long p = 0; p < (unsigned long long)g.npoints; ++p) {
-    decode(g, p, z);
     if (!exec_point<0>(g, z, c3)) break;
+    // next point in lexicographic order (odometer: no 64-bit divisions)
+    for (int i = g.nidx - 1; i >= 0; --i) {
+      if (++z[i] < g.lo[i] + g.ext[i]) break;
+      z[i] = g.lo[i];
+    }
   }
   g.cnt[0] = c3[0];
   g.cnt[1] = c3[1];
@@ -417,6 +448,8 @@ struct GenericPlan {
   int64_t* d_fbase = nullptr;
   int64_t* d_sbase = nullptr;
   int64_t* d_lsize = nullptr;
+  int* d_is_input = nullptr;
+  unsigned bad = 0;  // why the dataflow grid was declined (order-check bits)
   long long* d_shadow = nullptr;
   unsigned* d_flags = nullptr;
   unsigned* d_flags0 = nullptr;  // initial flags (dataflow)
@@ -684,6 +717,11 @@ GenericPlan* generic_plan_create(const KernelSpec& k, const IntVec& prm,
   P->d_fbase = upload(P->fbase);
   P->d_sbase = upload(P->sbase);
   P->d_lsize = upload(P->lsizes);
+  {
+    std::vector<int> inp;
+    for (auto kd : P->kinds) inp.push_back(kd == ArrayKind::Input ? 1 : 0);
+    P->d_is_input = upload(inp);
+  }
   if (P->mapped)
     ckc(cudaMalloc(&P->d_shadow, std::max<int64_t>(P->nshadow, 1) * sizeof(long long)), "cudaMalloc");
   ckc(cudaMalloc(&P->d_flags, std::max<int64_t>(P->nflags, 1) * sizeof(unsigned)), "cudaMalloc");
@@ -706,6 +744,7 @@ void generic_plan_destroy(GenericPlan* p) {
   cudaFree(p->d_fbase);
   cudaFree(p->d_sbase);
   cudaFree(p->d_lsize);
+  cudaFree(p->d_is_input);
   cudaFree(p->d_shadow);
   cudaFree(p->d_flags);
   cudaFree(p->d_flags0);
@@ -752,6 +791,7 @@ static GDev dev_args(GenericPlan* p) {
   g.lsize = p->d_lsize;
   g.shadow = p->d_shadow;
   g.never_ok = p->mapped ? 0 : 1;
+  g.is_input = p->d_is_input;
   g.flags = p->d_flags;
   g.next = p->d_misc;
   g.cnt = p->d_misc + 1;
@@ -807,6 +847,11 @@ cudaError_t generic_run(GenericPlan* p, cudaStream_t s, GenericCounts* counts, s
     cudaFree(p->d_writer);  // only the counting pass needs it
     p->d_writer = nullptr;
     p->dataflow = maxc[0] <= 1 && maxc[1] == 0;
+    p->bad = maxc[1] | (maxc[0] > 1 ? 16u : 0u);
+    if (env_int("PCOTGPU_GENERIC_DEBUG", 0))
+      std::fprintf(stderr, "generic: mapped=%d logical=%lld storage=%lld max_writes=%u order_bits=%u -> %s\n",
+                   int(p->mapped), (long long)p->nflags, (long long)p->nshadow, maxc[0], maxc[1],
+                   p->dataflow ? (p->mapped ? "dataflow (shadows)" : "dataflow (flags)") : "sequential");
     if ((e = cudaMemcpyAsync(p->d_flags0, p->d_flags, std::max<int64_t>(p->nflags, 1) * sizeof(unsigned),
                              cudaMemcpyDeviceToDevice, s)) != cudaSuccess)
       return e;
@@ -827,12 +872,26 @@ cudaError_t generic_run(GenericPlan* p, cudaStream_t s, GenericCounts* counts, s
   if (p->npoints > 0) {
     if (p->dataflow && p->mapped) {
       generic_dataflow_kernel<2><<<sms * 4, 128, 0, s>>>(g);
+      count_launch();
+      // a storage cell reused under a waiting reader (the map folds along a
+      // vector that is not universal for this kernel's dependences): this run
+      // is void; the plan switches to the reference's sequential order for
+      // good and the run is repeated from the initial storage
+      int e2 = 0;
+      if ((e = cudaMemcpyAsync(&e2, p->d_err, sizeof(int), cudaMemcpyDeviceToHost, s)) != cudaSuccess) return e;
+      if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return e;
+      if (e2 == -2) {
+        p->dataflow = false;
+        if (env_int("PCOTGPU_GENERIC_DEBUG", 0))
+          std::fprintf(stderr, "generic: storage reuse race detected -> sequential\n");
+        return generic_run(p, s, counts, err_msg);
+      }
     } else if (p->dataflow) {
       generic_dataflow_kernel<1><<<sms * 4, 128, 0, s>>>(g);
     } else {
       generic_sequential_kernel<<<1, 32, 0, s>>>(g);
     }
-    count_launch();
+    if (!(p->dataflow && p->mapped)) count_launch();
   }
   unsigned long long c[3] = {0, 0, 0};
   int err = 0;
@@ -852,6 +911,7 @@ cudaError_t generic_run(GenericPlan* p, cudaStream_t s, GenericCounts* counts, s
     counts->reads = c[1];
     counts->writes = c[2];
     counts->parallel = p->dataflow;
+    counts->mode = !p->dataflow ? 0 : p->mapped ? 2 : 1;
   }
   return cudaSuccess;
 }

@@ -63,6 +63,7 @@ cudaError_t generic_init_inputs(GenericPlan* p, cudaStream_t s);
 struct GenericCounts {
   uint64_t points = 0, reads = 0, writes = 0;
   bool parallel = false;  // dataflow grid (true) or sequential walk
+  int mode = 0;           // 0 sequential, 1 dataflow over dense flags, 2 dataflow over shadows
 };
 // One run.  Errors: cudaErrorInvalidValue with `err_msg` set for an
 // out-of-extent access (reference exec.cpp:318-323).

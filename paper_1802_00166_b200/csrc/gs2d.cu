@@ -771,6 +771,277 @@ __global__ void __launch_bounds__(NW * 32, 1) gs2d_pipe_kernel(PipeArgs g) {
 
 }  // namespace pipe
 
+// ---------------------------------------------------------------------------
+// Systolic pipeline, K levels per warp (v2).  Same bands, drifting windows,
+// edge slots, rings and wrap buffers as gs2d_pipe_kernel, but every warp
+// carries K consecutive levels t0 .. t0+K-1 in registers: lane l at clock c
+// updates, for every kk, row i0 - (t0+kk-1) + l at column c - 2l - 2kk.  Level
+// kk+1 then needs only values its own lane or its upper neighbour produced at
+// least one clock earlier:
+//   A (t, r-1, j-1..j+1): upper neighbour, level kk, clocks c-3..c-1;
+//   B (t, r, j-1):        own output, clock c-1;
+//   C (t-1, r, j..j+1):   upper neighbour, level kk-1, clocks c-4, c-3;
+//   D (t-1, r+1, j-1..j+1): own level kk-1 outputs, clocks c-3..c-1;
+// so the K updates of a clock are independent (K-way ILP), and ONE rotate
+// shuffle per level and clock feeds both the A and (four clocks later) the C
+// terms.  Lane 31 sends, instead of its own output (which no lane of the warp
+// needs), the band-above value lane 0 needs, so lane 0 takes the same path.
+// Level kk = 0 reads its C / D terms from the producer warp's ring (or warp
+// 0's staged rows) exactly as the one-level kernel does.  Per update: 12 fp64
+// operations + one shuffle + a few selects and predicated stores, against ~80
+// instructions of the one-level kernel, whose per-chunk overhead (edge resolve,
+// staging, progress) is now shared by K levels.
+namespace pipe2 {
+
+using pipe::PipeArgs;
+using pipe::BIG;
+using pipe::IRS;
+using pipe::SG;
+
+template <int NW, int K, int RS, int S>
+__global__ void __launch_bounds__(NW * 32, 1) gs2d_pipe2_kernel(PipeArgs g) {
+  static_assert(S + 2 <= SG / 2 && 3 * S + 4 <= IRS && S % 2 == 0, "chunk size");
+  static_assert((K + 1) * S <= 96, "edge slots per chunk: at most three per lane");
+  constexpr int RSP = RS + 1;
+  constexpr int L = NW * K;  // levels per pass
+  constexpr int XS = ((K + 1) * S + 31) / 32;  // edge slots per lane per chunk
+  extern __shared__ __align__(16) double sm[];
+  double* rb = sm;                          // [NW][32][RSP] last-level rings
+  double* ir = rb + NW * 32 * RSP;          // [32][IRS] warp 0's staged rows
+  double* above = ir + 32 * IRS;            // [NW][K][SG] band b-1's last row per level
+  double* cabove = above + NW * K * SG;     // [NW][SG] same row, level t0 - 1
+  volatile int* prog = reinterpret_cast<volatile int*>(cabove + NW * SG);  // [NW]
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, b = blockIdx.x;
+  const int i0 = 1 + 32 * b;
+  const bool has_above = b > 0;
+  if (lane == 0) prog[w] = 0;
+  __syncthreads();
+  double* myring = rb + (w * 32 + lane) * RSP;
+  double* const ab = above + w * K * SG;
+  double* const cab = cabove + w * SG;
+  const double* prowD = w ? rb + ((w - 1) * 32 + lane) * RSP : ir + lane * IRS;
+  const double* prowC = lane == 0 ? cab
+                                  : (w ? rb + ((w - 1) * 32 + lane - 1) * RSP : ir + (lane - 1) * IRS);
+  const int dmask = w ? RS - 1 : IRS - 1;
+  const int cmask = lane == 0 ? SG - 1 : dmask;
+  const int src_lane = (lane + 31) & 31;  // rotate: lane 0 hears lane 31
+  const int nclk = g.n + 63 + 2 * (K - 1);   // clocks -1 .. n + 61 + 2(K-1)
+  const int nchunk = (nclk + S - 1) / S;
+  const int fin = nchunk * S - 1;            // every warp publishes at most fin
+  auto need = [&](int v) { return v < fin ? v : fin; };
+  int seen_prod = 0, seen_cons = 0, seen_wrap = 0;
+  for (int p = 0;; ++p) {
+    const int t0 = p * L + w * K + 1;  // this warp's first level in pass p
+    if (t0 > g.T) break;
+    const int plv = (p + 1) * BIG;     // progress base of pass p
+    const bool cons_live = w < NW - 1 && t0 + K <= g.T;  // consumer warp has pass p
+    const double* src0 = ((p - 1) & 1) ? g.wb[1] : g.wb[0];  // warp 0, p > 0
+    double* wb_out = (p & 1) ? g.wb[1] : g.wb[0];             // warp NW-1
+    // ---- edge slots of this pass: (K+1) rows x S columns per chunk
+    // slot m: row kk = m / S - 1 (-1: level t0 - 1 for lane 0's C at kk = 0),
+    // column offset m % S
+    const double* xrow[XS];
+    int xoff[XS];
+    bool xlive[XS], xpoll[XS];
+    double* xdst[XS];
+#pragma unroll
+    for (int x = 0; x < XS; ++x) {
+      const int m = lane + 32 * x;
+      const int kk = m / S - 1, o = m % S;
+      const bool slot = m < (K + 1) * S;
+      const int t = t0 + kk;  // level of the row
+      const double* row = g.eb + (int64_t(t - 1) * g.nb + (b - 1)) * g.ebld;
+      bool live, poll;
+      if (kk < 0) {  // lane 0's C at kk = 0: band b-1's last row at t0-1, or the input row i0
+        live = slot && (t0 == 1 ? i0 <= g.n - 1 : has_above);
+        poll = live && t0 > 1;
+        if (t0 == 1) row = g.a + int64_t(i0) * g.ld;
+        xoff[x] = o;             // columns kS .. kS + S - 1
+        xdst[x] = cab;
+      } else {       // lane 31's send for level kk: columns kS + 1 - 2kk ..
+        live = slot && has_above && t <= g.T;
+        poll = live;
+        xoff[x] = o + 1 - 2 * kk;
+        xdst[x] = ab + kk * SG;
+      }
+      xrow[x] = row;
+      xlive[x] = live;
+      xpoll[x] = poll;
+    }
+    auto xload = [&](int k, double* v) {
+#pragma unroll
+      for (int x = 0; x < XS; ++x) {
+        const int col = k * S + xoff[x];
+        v[x] = 0.0;
+        if (xlive[x] && col >= 0 && col < g.n) v[x] = xpoll[x] ? pipe::ld_relaxed(xrow[x] + col) : xrow[x][col];
+      }
+    };
+    auto xresolve = [&](int k, double* v) {
+      unsigned ns = 16;
+#pragma unroll
+      for (int x = 0; x < XS; ++x) {
+        const int col = k * S + xoff[x];
+        const bool mine = xpoll[x] && col >= 0 && col < g.n;
+        long long it = 0;
+        for (; __any_sync(0xffffffffu, mine && pipe::is_empty(v[x])) && it < pipe::kSpinCap; ++it) {
+          if (g.spin_ns) __nanosleep(ns);
+          ns = ns * 2 < unsigned(g.spin_ns) ? ns * 2 : unsigned(g.spin_ns);
+          if (mine && pipe::is_empty(v[x])) v[x] = pipe::ld_relaxed(xrow[x] + col);
+        }
+        if (it == pipe::kSpinCap) pipe::spin_fault(g.err);
+        if (lane + 32 * x < (K + 1) * S) xdst[x][col & (SG - 1)] = v[x];
+      }
+    };
+    // ---- warp 0: level t0-1 rows (input grid or the wrap buffer), as v1
+    const int srow = i0 - t0 + 2 + lane;
+    const bool srow_ok = srow >= 0 && srow <= g.n - 1;
+    const double* const srcrow = (t0 == 1 ? g.a : src0) + int64_t(srow) * g.ld;
+    double* const irow = ir + lane * IRS;
+    auto load_pair = [&](int k, int m) {
+      const int pp = k * S - 2 - 2 * lane + 2 * m;
+      double2 v = make_double2(0.0, 0.0);
+      if (srow_ok && pp >= 0 && pp < g.n) v = __ldcg(reinterpret_cast<const double2*>(srcrow + pp));
+      return v;
+    };
+    auto store_pair = [&](int k, int m, double2 v) {
+      const int pp = k * S - 2 - 2 * lane + 2 * m;
+      if (pp >= 0 && pp < g.n) *reinterpret_cast<double2*>(irow + (pp & (IRS - 1))) = v;
+    };
+    double2 pre[S / 2];
+    if (w == 0) {
+      if (p > 0) pipe::wait_smem(prog + NW - 1, p * BIG + need(S + 2 * (K - 1)), g.err);
+      store_pair(0, 0, load_pair(0, 0));
+#pragma unroll
+      for (int m = 1; m <= S / 2; ++m) pre[m - 1] = load_pair(0, m);
+    }
+    // ---- per-level roles
+    bool row_ok[K];
+    double* orow[K];
+    double* erow[K];
+    unsigned ofull = 0;  // bit kk: level kk writes every in-range column (wrap buffer)
+    unsigned olast = 0;  // bit kk: level kk is t = T (result in place, updated cells)
+#pragma unroll
+    for (int kk = 0; kk < K; ++kk) {
+      const int t = t0 + kk;
+      const int i = i0 - (t - 1) + lane;
+      row_ok[kk] = t <= g.T && i >= 1 && i <= g.n - 2;
+      const bool last = t == g.T;
+      const bool wrap = w == NW - 1 && kk == K - 1 && t < g.T && i >= 0 && i <= g.n - 1;
+      orow[kk] = (last ? g.a : wb_out) + int64_t(i) * g.ld;
+      erow[kk] = g.eb + (int64_t(t - 1) * g.nb + b) * g.ebld;
+      if (last) olast |= 1u << kk;
+      if (wrap) ofull |= 1u << kk;
+    }
+    const bool elive = lane == 31;
+    // ---- register state: h[kk][0..3] = stream (upper neighbour) at c-1..c-4,
+    // o[kk][0..2] = own outputs at c-1..c-3; level 0's ring terms
+    double h[K][4], o[K][3];
+#pragma unroll
+    for (int kk = 0; kk < K; ++kk) {
+      h[kk][0] = h[kk][1] = h[kk][2] = h[kk][3] = 0.0;
+      o[kk][0] = o[kk][1] = o[kk][2] = 0.0;
+    }
+    double c1 = 0, c2 = 0, d1 = 0, d2 = 0, d3 = 0;
+    double xv[XS];
+    xload(0, xv);
+    for (int k = 0; k < nchunk; ++k) {
+      const int c_lo = k * S - 1;
+      const int c_hi = c_lo + S - 1;
+      xresolve(k, xv);
+      if (w == 0) {
+#pragma unroll
+        for (int m = 1; m <= S / 2; ++m) store_pair(k, m, pre[m - 1]);
+        if (k + 1 < nchunk) {
+          if (p > 0) pipe::wait_seen(prog + NW - 1, p * BIG + need(c_hi + S + 2 + 2 * (K - 1)), seen_wrap, g.err);
+#pragma unroll
+          for (int m = 1; m <= S / 2; ++m) pre[m - 1] = load_pair(k + 1, m);
+        }
+      }
+      // producer's last level ahead of our level 0 (its column j+1 at our clock c)
+      if (w > 0) pipe::wait_seen(prog + w - 1, plv + need(c_hi + 2 + 2 * (K - 1)), seen_prod, g.err);
+      if (w < NW - 1) {
+        // ring reuse (our last level writes column c - 2l - 2(K-1) into slot mod RS)
+        const int rel = c_hi + 6 - RS - 2 * (K - 1);
+        if (rel > 0 && cons_live) {
+          pipe::wait_seen(prog + w + 1, plv + need(rel), seen_cons, g.err);
+        } else if (p > 0) {
+          pipe::wait_seen(prog + w + 1, p * BIG + fin, seen_cons, g.err);
+        }
+      }
+      __syncwarp();
+      unsigned upd[K], inb[K];
+#pragma unroll
+      for (int kk = 0; kk < K; ++kk) {
+        const int j0 = c_lo - 2 * lane - 2 * kk;
+        inb[kk] = pipe::span_mask<S>(j0, 0, g.n - 1);
+        upd[kk] = row_ok[kk] ? pipe::span_mask<S>(j0, 1, g.n - 2) : 0u;
+      }
+      const int jr = c_lo - 2 * lane - 2 * (K - 1);  // last level's column at the chunk start
+#pragma unroll
+      for (int cc = 0; cc < S; ++cc) {
+        if (cc == pipe::kXLoadClock && k + 1 < nchunk) xload(k + 1, xv);
+        const int c = c_lo + cc;
+        // level 0's producer terms (columns j..j+1 from lane l-1, j-1..j+1 from lane l)
+        const int q = c - 2 * lane + 1;  // level 0: j + 1
+        c1 = c2;
+        c2 = prowC[q & cmask];
+        d1 = d2;
+        d2 = d3;
+        d3 = prowD[q & dmask];
+        double nv[K];
+#pragma unroll
+        for (int kk = 0; kk < K; ++kk) {
+          const double A1 = h[kk][2], A2 = h[kk][1], A3 = h[kk][0];
+          const double C1 = kk ? h[kk - 1][3] : c1, C2 = kk ? h[kk - 1][2] : c2;
+          const double D1 = kk ? o[kk - 1][2] : d1, D2 = kk ? o[kk - 1][1] : d2,
+                       D3 = kk ? o[kk - 1][0] : d3;
+          double s = add(A1, A2);
+          s = add(s, A3);
+          s = add(s, o[kk][0]);
+          s = add(s, C1);
+          s = add(s, C2);
+          s = add(s, D1);
+          s = add(s, D2);
+          s = add(s, D3);
+          const double r = div9(s);
+          nv[kk] = (upd[kk] >> cc) & 1u ? r : 0.0;
+        }
+        // stores: edge slot (lane 31), result / wrap buffer, ring (last level)
+#pragma unroll
+        for (int kk = 0; kk < K; ++kk) {
+          const int j = c - 2 * lane - 2 * kk;
+          const double v = nv[kk];
+          if (elive && ((inb[kk] >> cc) & 1u))
+            pipe::st_relaxed(erow[kk] + j, pipe::is_empty(v) ? __longlong_as_double(0x7fffffffffffffffLL) : v);
+          const unsigned om = ((olast >> kk) & 1u) ? upd[kk] : (((ofull >> kk) & 1u) ? inb[kk] : 0u);
+          if ((om >> cc) & 1u) orow[kk][j] = v;
+        }
+        myring[(jr + cc) & (RS - 1)] = nv[K - 1];
+        // shift histories; one rotate shuffle per level (lane 31 sends lane 0's
+        // band-above value for the column lane 0 needs next clock)
+#pragma unroll
+        for (int kk = 0; kk < K; ++kk) {
+          o[kk][2] = o[kk][1];
+          o[kk][1] = o[kk][0];
+          o[kk][0] = nv[kk];
+          const double send = lane == 31 ? ab[kk * SG + ((c + 2 - 2 * kk) & (SG - 1))] : nv[kk];
+          const double in = __shfl_sync(0xffffffffu, send, src_lane);
+          h[kk][3] = h[kk][2];
+          h[kk][2] = h[kk][1];
+          h[kk][1] = h[kk][0];
+          h[kk][0] = in;
+        }
+      }
+      __syncwarp();
+      if (lane == 0) pipe::st_release_cta(prog + w, plv + c_hi + 1);
+      __syncwarp();
+    }
+    __syncwarp();
+  }
+}
+
+}  // namespace pipe2
+
 // 2: line-group warp kernel (4 x 32 lines), 1: one-warp tile, 0: CTA tile
 int gs_kind(int bt, int bx) {
   if (bt == lines::BT && bx == lines::BX) return 2;
@@ -886,17 +1157,22 @@ void gs2d_plan_destroy(GsPlan* p) {
   delete p;
 }
 
-// Pipeline variants: {warps (levels) per CTA, ring depth, clocks per chunk}.
+// Pipeline variants: {warps per CTA, ring depth, clocks per chunk, levels per
+// warp (1: gs2d_pipe_kernel, K > 1: gs2d_pipe2_kernel)}.
 struct PipeVariant {
-  int nw, rs, s;
+  int nw, rs, s, k;
   void (*kern)(pipe::PipeArgs);
 };
 const PipeVariant kPipeVariants[] = {
-    {16, 32, 8, pipe::gs2d_pipe_kernel<16, 32, 8>},
-    {12, 64, 8, pipe::gs2d_pipe_kernel<12, 64, 8>},
-    {8, 64, 8, pipe::gs2d_pipe_kernel<8, 64, 8>},
-    {12, 64, 4, pipe::gs2d_pipe_kernel<12, 64, 4>},
-    {12, 64, 16, pipe::gs2d_pipe_kernel<12, 64, 16>},
+    {16, 32, 8, 1, pipe::gs2d_pipe_kernel<16, 32, 8>},
+    {12, 64, 8, 1, pipe::gs2d_pipe_kernel<12, 64, 8>},
+    {8, 64, 8, 1, pipe::gs2d_pipe_kernel<8, 64, 8>},
+    {12, 64, 4, 1, pipe::gs2d_pipe_kernel<12, 64, 4>},
+    {12, 64, 16, 1, pipe::gs2d_pipe_kernel<12, 64, 16>},
+    {8, 64, 8, 8, pipe2::gs2d_pipe2_kernel<8, 8, 64, 8>},
+    {4, 64, 8, 8, pipe2::gs2d_pipe2_kernel<4, 8, 64, 8>},
+    {8, 64, 8, 4, pipe2::gs2d_pipe2_kernel<8, 4, 64, 8>},
+    {16, 32, 8, 4, pipe2::gs2d_pipe2_kernel<16, 4, 32, 8>},
 };
 constexpr int kNumPipeVariants = sizeof(kPipeVariants) / sizeof(kPipeVariants[0]);
 const PipeVariant& pipe_variant() {
@@ -907,6 +1183,9 @@ const PipeVariant& pipe_variant() {
 
 size_t gs2d_pipe_smem(const PipeVariant& v) {
   using namespace pipe;
+  if (v.k > 1)  // rings, staged rows, K band-above rows + the level t0-1 row per warp, progress
+    return size_t(v.nw) * 32 * (v.rs + 1) * 8 + size_t(32) * IRS * 8 + size_t(v.k + 1) * v.nw * SG * 8 +
+           v.nw * 4;
   return size_t(v.nw) * 32 * (v.rs + 1) * 8 + size_t(32) * IRS * 8 + size_t(2) * v.nw * SG * 8 +
          v.nw * 4;
 }

@@ -129,6 +129,7 @@ int main(int argc, char** argv) {
     pcot::GpuExecutor gx(e, params, maps);
     const pcot::ExecResult g = scheme == "untiled" ? gx.run_untiled() : gx.run(order);
     std::printf("GPU_FAMILY %d\n", gx.family());
+    std::printf("GPU_MODE %d\n", gx.last_bt());
     std::printf("GPU_CHECKSUM %016" PRIx64 "\n", g.checksum);
     std::printf("GPU_COUNTS %" PRIu64 " %" PRIu64 " %" PRIu64 "\n", g.points, g.reads, g.writes);
     for (const auto& a : e.arrays)

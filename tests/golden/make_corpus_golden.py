@@ -31,6 +31,29 @@ CASES = [
 ]
 
 
+# Large sizes under allocate()'s memory maps (the folded storage the
+# reference's CLI uses with --alloc): the reference's emitted C (emit_c
+# use_alloc, -O2 -ffp-contract=off -fopenmp), which the reference asserts is
+# bit-identical to its interpreter (tests/acceptance.cpp:662-711).
+MAPPED = [("lud", {"N": 512}), ("osp", {"N": 256}), ("triangle", {"N": 4096}),
+          ("heat1d-fig7", {"T": 2048, "N": 8192})]
+
+
+def run_emitted(name, params):
+    import re
+
+    env = dict(os.environ, PCOT_KERNEL_PATH=CORPUS, OMP_NUM_THREADS=str(os.cpu_count() or 8))
+    ps = ",".join("%s=%d" % kv for kv in params.items())
+    with tempfile.TemporaryDirectory() as d:
+        c, b = os.path.join(d, "k.c"), os.path.join(d, "k")
+        subprocess.run([REF_BIN, "emit", name, ps, "--openmp", "-o", c], check=True, env=env)
+        gcc = "/usr/bin/gcc" if os.path.exists("/usr/bin/gcc") else "gcc"
+        subprocess.run([gcc, "-std=c99", "-O2", "-ffp-contract=off", "-fopenmp", c, "-lm", "-o", b],
+                       check=True)
+        out = subprocess.run([b], capture_output=True, text=True, env=env, check=True).stdout
+    return re.search(r"CHECKSUM ([0-9a-f]{16})", out).group(1)
+
+
 def run(name, params, dump):
     env = dict(os.environ, PCOT_KERNEL_PATH=CORPUS)
     ps = ",".join("%s=%d" % kv for kv in params.items())
@@ -55,11 +78,17 @@ def main():
                 e["out_hex"] = ["%016x" % v for v in struct.unpack("<%dQ" % (len(raw) // 8), raw)]
             entries.append(e)
             print(name, params, e["checksum"], e["points"])
+    mapped = []
+    for name, params in MAPPED:
+        chk = run_emitted(name, params)
+        mapped.append({"kernel": name, "params": params, "checksum": chk, "maps": "allocate",
+                       "source": "reference emitted C (emit_c use_alloc, OpenMP)"})
+        print(name, params, chk, "(allocate maps)")
     with open(OUT, "w") as f:
         json.dump({"generator": "tests/golden/make_corpus_golden.py",
                    "reference": "oracle/_ref/pcot_ref run <kernel> --scheme untiled (single-assignment "
                                 "storage; /root/reference/proj/kernels)",
-                   "entries": entries}, f, indent=1)
+                   "entries": entries, "mapped": mapped}, f, indent=1)
 
 
 if __name__ == "__main__":

@@ -146,3 +146,30 @@ def test_interpreter_honours_a_folded_map(fold):
         assert r.checksum_hex == want
         assert ex.array_words("X") == fold * N * N
         assert ex.array_base("Out") == 64 + (N * N * 8 + 63) // 64 * 64 + (fold * N * N * 8 + 63) // 64 * 64
+
+
+def _mapped_cases():
+    import json
+
+    with open(os.path.join(O.REPO, "tests", "golden", "corpus.json")) as f:
+        return json.load(f).get("mapped", [])
+
+
+MAPPED = _mapped_cases()
+
+
+@pytest.mark.gpu
+@need_demo
+@pytest.mark.parametrize("e", MAPPED, ids=["%s-%s" % (e["kernel"], "-".join("%s%d" % kv for kv in e["params"].items()))
+                                           for e in MAPPED])
+def test_large_corpus_kernels_from_allocate_mapped_storage(e):
+    """lud / osp / triangle / heat1d-fig7 at sizes whose
+    single-assignment storage would not be the point (lud N=512: A folded from
+    N^3 to ~2N^2 words), run on the device from allocate()'s maps through the
+    reference-side adapter, against the reference's emitted-C checksum."""
+    ps = ",".join("%s=%d" % kv for kv in e["params"].items())
+    rc, out, txt = _demo([os.path.join(KDIR, e["kernel"] + ".kernel"), ps, "--gpu-only"], timeout=900)
+    assert rc == 0, txt
+    assert int(out["GPU_FAMILY"][0]) == 5
+    assert out["GPU_CHECKSUM"] == [e["checksum"]], txt
+    assert out["GPU_RERUN_CHECKSUM"] == [e["checksum"]]
