@@ -180,8 +180,16 @@ PCOT_DEV bool exec_point(const GDev& g, const int64_t* z, unsigned long long* c3
             // wait until the storage cell holds this logical cell's value ...
             const long long want = logical_of(g, r, z);
             const long long* sh = g.shadow + g.sbase[r.array] + f;
+            const unsigned long long* wk = g.writer + g.fbase[r.array];
             long long it = 0;
-            while (ld_acq_s64(sh) != want) {
+            for (long long held; (held = ld_acq_s64(sh)) != want;) {
+              // the cell holds a LATER occupant (its write comes after ours in
+              // the reference's order): our value was overwritten before this
+              // read — the fold is not universal for this kernel
+              if (held >= 0 && wk[held] > wk[want]) {
+                atomicCAS(g.err, 0, -2);
+                return false;
+              }
               if (++it > kSpinCapG) {
                 atomicCAS(g.err, 0, -1);
                 return false;
@@ -792,6 +800,7 @@ static GDev dev_args(GenericPlan* p) {
   g.shadow = p->d_shadow;
   g.never_ok = p->mapped ? 0 : 1;
   g.is_input = p->d_is_input;
+  g.writer = p->d_writer;  // mapped dataflow: writer keys of the logical cells
   g.flags = p->d_flags;
   g.next = p->d_misc;
   g.cnt = p->d_misc + 1;
@@ -844,8 +853,10 @@ cudaError_t generic_run(GenericPlan* p, cudaStream_t s, GenericCounts* counts, s
       if (err_msg) *err_msg = "out-of-extent write in statement " + p->stmt_ids[size_t(err - 1)];
       return cudaErrorInvalidValue;
     }
-    cudaFree(p->d_writer);  // only the counting pass needs it
-    p->d_writer = nullptr;
+    if (!p->mapped) {  // dense storage: only the counting pass needs the writer keys
+      cudaFree(p->d_writer);
+      p->d_writer = nullptr;
+    }
     p->dataflow = maxc[0] <= 1 && maxc[1] == 0;
     p->bad = maxc[1] | (maxc[0] > 1 ? 16u : 0u);
     if (env_int("PCOTGPU_GENERIC_DEBUG", 0))

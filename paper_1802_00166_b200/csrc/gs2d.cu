@@ -536,6 +536,19 @@ PCOT_DEV void st_relaxed(double* p, double v) {
 }
 PCOT_DEV bool is_empty(double v) { return __double_as_longlong(v) == kEmpty; }
 
+// Predicated stores without a branch (SASS @P STG): a per-lane `if` around a
+// store inside the clock loop makes the warp diverge, and every later shuffle
+// then takes the compiler's collective slow path (WARPSYNC / ENDCOLLECTIVE).
+PCOT_DEV void st_relaxed_if(double* p, double v, bool pred) {
+  asm volatile(
+      "{\n .reg .pred q;\n setp.ne.b32 q, %2, 0;\n @q st.relaxed.gpu.global.f64 [%0], %1;\n}" ::"l"(p),
+      "d"(v), "r"(int(pred)));
+}
+PCOT_DEV void st_global_if(double* p, double v, bool pred) {
+  asm volatile("{\n .reg .pred q;\n setp.ne.b32 q, %2, 0;\n @q st.global.f64 [%0], %1;\n}" ::"l"(p),
+               "d"(v), "r"(int(pred)));
+}
+
 // Bits kk in [0, S) with lo <= j0 + kk <= hi.
 template <int S>
 PCOT_DEV unsigned span_mask(int j0, int lo, int hi) {
@@ -737,8 +750,8 @@ __global__ void __launch_bounds__(NW * 32, 1) gs2d_pipe_kernel(PipeArgs g) {
         myring[(j0 + kk) & (RS - 1)] = v;
         // lane 31: the band's last row (a computed NaN carrying the kEmpty bit
         // pattern would read as "not yet written": stored as the canonical NaN)
-        if ((emask >> kk) & 1u) st_relaxed(ep + kk, is_empty(v) ? __longlong_as_double(0x7fffffffffffffffLL) : v);
-        if ((omask >> kk) & 1u) op[kk] = v;              // result / wrap buffer
+        st_relaxed_if(ep + kk, is_empty(v) ? __longlong_as_double(0x7fffffffffffffffLL) : v, (emask >> kk) & 1u);
+        st_global_if(op + kk, v, (omask >> kk) & 1u);  // result / wrap buffer
       }
       PCOT_PROF(5);
 #ifdef PCOT_EDGE_FENCE
@@ -808,7 +821,7 @@ __global__ void __launch_bounds__(NW * 32, 1) gs2d_pipe2_kernel(PipeArgs g) {
   extern __shared__ __align__(16) double sm[];
   double* rb = sm;                          // [NW][32][RSP] last-level rings
   double* ir = rb + NW * 32 * RSP;          // [32][IRS] warp 0's staged rows
-  double* above = ir + 32 * IRS;            // [NW][K][SG] band b-1's last row per level
+  double* above = ir + 32 * IRS;            // [NW][2][K][S] band b-1's last row per level (chunk-relative)
   double* cabove = above + NW * K * SG;     // [NW][SG] same row, level t0 - 1
   volatile int* prog = reinterpret_cast<volatile int*>(cabove + NW * SG);  // [NW]
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, b = blockIdx.x;
@@ -817,7 +830,7 @@ __global__ void __launch_bounds__(NW * 32, 1) gs2d_pipe2_kernel(PipeArgs g) {
   if (lane == 0) prog[w] = 0;
   __syncthreads();
   double* myring = rb + (w * 32 + lane) * RSP;
-  double* const ab = above + w * K * SG;
+  double* const ab = above + w * K * SG;  // (SG >= 2S: the [2][K][S] staging fits the same space)
   double* const cab = cabove + w * SG;
   const double* prowD = w ? rb + ((w - 1) * 32 + lane) * RSP : ir + lane * IRS;
   const double* prowC = lane == 0 ? cab
@@ -830,6 +843,17 @@ __global__ void __launch_bounds__(NW * 32, 1) gs2d_pipe2_kernel(PipeArgs g) {
   const int fin = nchunk * S - 1;            // every warp publishes at most fin
   auto need = [&](int v) { return v < fin ? v : fin; };
   int seen_prod = 0, seen_cons = 0, seen_wrap = 0;
+  // optional cycle accounting (PCOTGPU_GS_PROF): same slots as the one-level kernel
+  long long pacc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  long long t_first = 0, c_first = 0;
+  const long long t_entry = g.prof ? globaltimer() : 0;
+  long long tp = 0;
+#define PCOT_PROF2(slot)            \
+  if (g.prof) {                     \
+    const long long now = clock64(); \
+    pacc[slot] += now - tp;         \
+    tp = now;                       \
+  }
   for (int p = 0;; ++p) {
     const int t0 = p * L + w * K + 1;  // this warp's first level in pass p
     if (t0 > g.T) break;
@@ -862,7 +886,7 @@ __global__ void __launch_bounds__(NW * 32, 1) gs2d_pipe2_kernel(PipeArgs g) {
         live = slot && has_above && t <= g.T;
         poll = live;
         xoff[x] = o + 1 - 2 * kk;
-        xdst[x] = ab + kk * SG;
+        xdst[x] = ab + kk * S + o;  // + (k & 1) * K * S: chunk-relative, double buffered
       }
       xrow[x] = row;
       xlive[x] = live;
@@ -889,7 +913,10 @@ __global__ void __launch_bounds__(NW * 32, 1) gs2d_pipe2_kernel(PipeArgs g) {
           if (mine && pipe::is_empty(v[x])) v[x] = pipe::ld_relaxed(xrow[x] + col);
         }
         if (it == pipe::kSpinCap) pipe::spin_fault(g.err);
-        if (lane + 32 * x < (K + 1) * S) xdst[x][col & (SG - 1)] = v[x];
+        if (lane + 32 * x < (K + 1) * S) {
+          if (lane + 32 * x < S) xdst[x][col & (SG - 1)] = v[x];  // cab: column-indexed (prowC)
+          else xdst[x][(k & 1) * K * S] = v[x];
+        }
       }
     };
     // ---- warp 0: level t0-1 rows (input grid or the wrap buffer), as v1
@@ -933,6 +960,7 @@ __global__ void __launch_bounds__(NW * 32, 1) gs2d_pipe2_kernel(PipeArgs g) {
       if (wrap) ofull |= 1u << kk;
     }
     const bool elive = lane == 31;
+    const bool has_out = __any_sync(0xffffffffu, (olast | ofull) != 0u);  // warp-uniform
     // ---- register state: h[kk][0..3] = stream (upper neighbour) at c-1..c-4,
     // o[kk][0..2] = own outputs at c-1..c-3; level 0's ring terms
     double h[K][4], o[K][3];
@@ -947,7 +975,9 @@ __global__ void __launch_bounds__(NW * 32, 1) gs2d_pipe2_kernel(PipeArgs g) {
     for (int k = 0; k < nchunk; ++k) {
       const int c_lo = k * S - 1;
       const int c_hi = c_lo + S - 1;
+      if (g.prof) tp = clock64();
       xresolve(k, xv);
+      PCOT_PROF2(0);
       if (w == 0) {
 #pragma unroll
         for (int m = 1; m <= S / 2; ++m) store_pair(k, m, pre[m - 1]);
@@ -957,8 +987,10 @@ __global__ void __launch_bounds__(NW * 32, 1) gs2d_pipe2_kernel(PipeArgs g) {
           for (int m = 1; m <= S / 2; ++m) pre[m - 1] = load_pair(k + 1, m);
         }
       }
+      PCOT_PROF2(1);
       // producer's last level ahead of our level 0 (its column j+1 at our clock c)
       if (w > 0) pipe::wait_seen(prog + w - 1, plv + need(c_hi + 2 + 2 * (K - 1)), seen_prod, g.err);
+      PCOT_PROF2(2);
       if (w < NW - 1) {
         // ring reuse (our last level writes column c - 2l - 2(K-1) into slot mod RS)
         const int rel = c_hi + 6 - RS - 2 * (K - 1);
@@ -968,7 +1000,12 @@ __global__ void __launch_bounds__(NW * 32, 1) gs2d_pipe2_kernel(PipeArgs g) {
           pipe::wait_seen(prog + w + 1, p * BIG + fin, seen_cons, g.err);
         }
       }
+      PCOT_PROF2(3);
       __syncwarp();
+      if (g.prof && t_first == 0) {
+        t_first = globaltimer();
+        c_first = clock64();
+      }
       unsigned upd[K], inb[K];
 #pragma unroll
       for (int kk = 0; kk < K; ++kk) {
@@ -977,6 +1014,19 @@ __global__ void __launch_bounds__(NW * 32, 1) gs2d_pipe2_kernel(PipeArgs g) {
         upd[kk] = row_ok[kk] ? pipe::span_mask<S>(j0, 1, g.n - 2) : 0u;
       }
       const int jr = c_lo - 2 * lane - 2 * (K - 1);  // last level's column at the chunk start
+      // per-chunk store bases (the clock index then becomes an immediate offset)
+      double* ep[K];
+      double* op[K];
+      unsigned om[K];  // result (level T: updated cells) / wrap buffer (every in-range cell)
+#pragma unroll
+      for (int kk = 0; kk < K; ++kk) {
+        const int j0 = c_lo - 2 * lane - 2 * kk;
+        ep[kk] = erow[kk] + j0;
+        op[kk] = orow[kk] + j0;
+        om[kk] = ((olast >> kk) & 1u) ? upd[kk] : (((ofull >> kk) & 1u) ? inb[kk] : 0u);
+        if (!elive) inb[kk] = 0u;  // edge-store mask: lane 31 only
+      }
+      const double* const abk = ab + (k & 1) * K * S;
 #pragma unroll
       for (int cc = 0; cc < S; ++cc) {
         if (cc == pipe::kXLoadClock && k + 1 < nchunk) xload(k + 1, xv);
@@ -988,33 +1038,38 @@ __global__ void __launch_bounds__(NW * 32, 1) gs2d_pipe2_kernel(PipeArgs g) {
         d1 = d2;
         d2 = d3;
         d3 = prowD[q & dmask];
+        // the K sums, operand by operand across the levels: K independent
+        // chains interleaved in issue order (the warp issues in order)
+        double sum[K];
+#pragma unroll
+        for (int kk = 0; kk < K; ++kk) sum[kk] = add(h[kk][2], h[kk][1]);
+#pragma unroll
+        for (int kk = 0; kk < K; ++kk) sum[kk] = add(sum[kk], h[kk][0]);
+#pragma unroll
+        for (int kk = 0; kk < K; ++kk) sum[kk] = add(sum[kk], o[kk][0]);
+#pragma unroll
+        for (int kk = 0; kk < K; ++kk) sum[kk] = add(sum[kk], kk ? h[kk - 1][3] : c1);
+#pragma unroll
+        for (int kk = 0; kk < K; ++kk) sum[kk] = add(sum[kk], kk ? h[kk - 1][2] : c2);
+#pragma unroll
+        for (int kk = 0; kk < K; ++kk) sum[kk] = add(sum[kk], kk ? o[kk - 1][2] : d1);
+#pragma unroll
+        for (int kk = 0; kk < K; ++kk) sum[kk] = add(sum[kk], kk ? o[kk - 1][1] : d2);
+#pragma unroll
+        for (int kk = 0; kk < K; ++kk) sum[kk] = add(sum[kk], kk ? o[kk - 1][0] : d3);
         double nv[K];
 #pragma unroll
         for (int kk = 0; kk < K; ++kk) {
-          const double A1 = h[kk][2], A2 = h[kk][1], A3 = h[kk][0];
-          const double C1 = kk ? h[kk - 1][3] : c1, C2 = kk ? h[kk - 1][2] : c2;
-          const double D1 = kk ? o[kk - 1][2] : d1, D2 = kk ? o[kk - 1][1] : d2,
-                       D3 = kk ? o[kk - 1][0] : d3;
-          double s = add(A1, A2);
-          s = add(s, A3);
-          s = add(s, o[kk][0]);
-          s = add(s, C1);
-          s = add(s, C2);
-          s = add(s, D1);
-          s = add(s, D2);
-          s = add(s, D3);
-          const double r = div9(s);
+          const double r = div9(sum[kk]);
           nv[kk] = (upd[kk] >> cc) & 1u ? r : 0.0;
         }
         // stores: edge slot (lane 31), result / wrap buffer, ring (last level)
 #pragma unroll
         for (int kk = 0; kk < K; ++kk) {
-          const int j = c - 2 * lane - 2 * kk;
           const double v = nv[kk];
-          if (elive && ((inb[kk] >> cc) & 1u))
-            pipe::st_relaxed(erow[kk] + j, pipe::is_empty(v) ? __longlong_as_double(0x7fffffffffffffffLL) : v);
-          const unsigned om = ((olast >> kk) & 1u) ? upd[kk] : (((ofull >> kk) & 1u) ? inb[kk] : 0u);
-          if ((om >> cc) & 1u) orow[kk][j] = v;
+          pipe::st_relaxed_if(ep[kk] + cc, pipe::is_empty(v) ? __longlong_as_double(0x7fffffffffffffffLL) : v,
+                              (inb[kk] >> cc) & 1u);
+          if (has_out) pipe::st_global_if(op[kk] + cc, v, (om[kk] >> cc) & 1u);
         }
         myring[(jr + cc) & (RS - 1)] = nv[K - 1];
         // shift histories; one rotate shuffle per level (lane 31 sends lane 0's
@@ -1024,7 +1079,7 @@ __global__ void __launch_bounds__(NW * 32, 1) gs2d_pipe2_kernel(PipeArgs g) {
           o[kk][2] = o[kk][1];
           o[kk][1] = o[kk][0];
           o[kk][0] = nv[kk];
-          const double send = lane == 31 ? ab[kk * SG + ((c + 2 - 2 * kk) & (SG - 1))] : nv[kk];
+          const double send = elive ? abk[kk * S + cc] : nv[kk];
           const double in = __shfl_sync(0xffffffffu, send, src_lane);
           h[kk][3] = h[kk][2];
           h[kk][2] = h[kk][1];
@@ -1032,11 +1087,26 @@ __global__ void __launch_bounds__(NW * 32, 1) gs2d_pipe2_kernel(PipeArgs g) {
           h[kk][0] = in;
         }
       }
+      PCOT_PROF2(5);
       __syncwarp();
       if (lane == 0) pipe::st_release_cta(prog + w, plv + c_hi + 1);
       __syncwarp();
+      PCOT_PROF2(6);
     }
     __syncwarp();
+  }
+#undef PCOT_PROF2
+  if (g.prof && lane == 0) {
+    long long* pr = g.prof + (int64_t(b) * NW + w) * 16;
+    for (int q = 0; q < 8; ++q) pr[q] = pacc[q];
+    pr[8] = t_first;
+    pr[9] = globaltimer();
+    pr[10] = c_first;
+    pr[11] = clock64();
+    pr[12] = t_entry;
+    unsigned smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    pr[13] = smid;
   }
 }
 
@@ -1169,10 +1239,10 @@ const PipeVariant kPipeVariants[] = {
     {8, 64, 8, 1, pipe::gs2d_pipe_kernel<8, 64, 8>},
     {12, 64, 4, 1, pipe::gs2d_pipe_kernel<12, 64, 4>},
     {12, 64, 16, 1, pipe::gs2d_pipe_kernel<12, 64, 16>},
-    {8, 64, 8, 8, pipe2::gs2d_pipe2_kernel<8, 8, 64, 8>},
-    {4, 64, 8, 8, pipe2::gs2d_pipe2_kernel<4, 8, 64, 8>},
+    {16, 32, 8, 2, pipe2::gs2d_pipe2_kernel<16, 2, 32, 8>},
+    {8, 64, 8, 2, pipe2::gs2d_pipe2_kernel<8, 2, 64, 8>},
     {8, 64, 8, 4, pipe2::gs2d_pipe2_kernel<8, 4, 64, 8>},
-    {16, 32, 8, 4, pipe2::gs2d_pipe2_kernel<16, 4, 32, 8>},
+    {4, 64, 8, 4, pipe2::gs2d_pipe2_kernel<4, 4, 64, 8>},
 };
 constexpr int kNumPipeVariants = sizeof(kPipeVariants) / sizeof(kPipeVariants[0]);
 const PipeVariant& pipe_variant() {

@@ -36,7 +36,7 @@ CASES = [
 # use_alloc, -O2 -ffp-contract=off -fopenmp), which the reference asserts is
 # bit-identical to its interpreter (tests/acceptance.cpp:662-711).
 MAPPED = [("lud", {"N": 512}), ("osp", {"N": 256}), ("triangle", {"N": 4096}),
-          ("heat1d-fig7", {"T": 2048, "N": 8192})]
+          ("heat1d-fig7", {"T": 256, "N": 2048})]
 
 
 def run_emitted(name, params):

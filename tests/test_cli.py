@@ -44,7 +44,7 @@ CASES = [
     ["heat3d_b", "-p", "T=5,N=19", "--alloc"],
     ["gs2d", "-p", "T=8,N=33", "--scheme", "cot", "--tile", "4,8,16", "--alloc"],
     ["lud", "-p", "N=40", "--alloc"],
-    ["osp", "-p", "N=30", "--scheme", "slt", "--tile", "4,4,4"],
+    ["osp", "-p", "N=30", "--scheme", "slt", "--tile", "4,4"],
     ["heat1d-fig7", "-p", "T=10,N=20", "--alloc"],
 ]
 
