@@ -24,6 +24,12 @@ enum class Scheme { Untiled, Slt, Cot };
 struct TileOrder {
   Scheme scheme = Scheme::Untiled;
   TileSpec tile;  // leaf sizes of the order (leaf[0]: time -> temporal block depth)
+  // COT only: the recursive order spans time too (reference cot_order recurses
+  // over the whole band box, t included, tiler.cpp:150-203): 2-D stencils run
+  // one launch per (depth block, row band of tile.leaf[1] rows), visited in
+  // Morton order over the skewed (block, band + 2 block) box, so a band goes
+  // through several depth blocks while it is L2-resident.
+  bool space_time = false;
 };
 
 // reference exec.hpp:40-52

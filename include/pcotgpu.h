@@ -43,7 +43,9 @@ enum pcotgpu_family {
 enum pcotgpu_scheme { PCOTGPU_UNTILED = 0, PCOTGPU_SLT = 1, PCOTGPU_COT = 2 };
 
 enum pcotgpu_run_flags {
-  PCOTGPU_SKIP_CHECKSUM = 1 /* leave result.checksum = 0 (no device->host copy) */
+  PCOTGPU_SKIP_CHECKSUM = 1, /* leave result.checksum = 0 (no device->host copy) */
+  PCOTGPU_SPACE_TIME = 2     /* COT on 2-D stencils: recursive order over (depth block,
+                                row band) across launches, bands of leaf[1] rows */
 };
 
 /* What the recognizer proved about a kernel at a parameter binding. */

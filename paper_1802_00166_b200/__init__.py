@@ -27,6 +27,7 @@ SCHEMES = {"untiled": 0, "slt": 1, "cot": 2}
 ERROR_KINDS = {1: "Overflow", 2: "DimMismatch", 3: "Unbounded", 4: "Parse", 5: "Validation",
                6: "Io", 7: "Unsupported", 8: "Cuda"}
 SKIP_CHECKSUM = 1
+SPACE_TIME = 2  # COT on 2-D stencils: recursive (depth block x row band) order across launches
 
 
 class PcotError(RuntimeError):
@@ -271,14 +272,16 @@ class GpuExecutor:
         self.close()
 
     @staticmethod
-    def _schedule(scheme, tile, skip_checksum):
+    def _schedule(scheme, tile, skip_checksum, space_time=False):
         s = Schedule()
+        if scheme == "cot-st":  # the space-time recursive order (TileOrder.space_time)
+            scheme, space_time = "cot", True
         s.scheme = SCHEMES[scheme] if isinstance(scheme, str) else int(scheme)
         tile = list(tile or [])
         s.ndim = len(tile)
         for i, v in enumerate(tile[:8]):
             s.leaf[i] = int(v)
-        s.flags = SKIP_CHECKSUM if skip_checksum else 0
+        s.flags = (SKIP_CHECKSUM if skip_checksum else 0) | (SPACE_TIME if space_time else 0)
         return s
 
     @property

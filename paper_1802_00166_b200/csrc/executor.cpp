@@ -247,6 +247,40 @@ struct GpuExecutor::Impl {
     const int order = o.scheme == Scheme::Cot ? kOrderMorton : kOrderLex;
     ck(copy_rows(sg[0].origin, sg[0].ld, in[0].p, in_ld, n, n, stream), "copy_rows");
     if (!rec.ring_hold) ck(zero_ring_2d(sg[0].origin, sg[0].ld, n, stream), "zero_ring");
+    if (o.scheme == Scheme::Cot && o.space_time && T > 0) {
+      // Space-time recursive order (reference cot_order over the band box with
+      // time, tiler.cpp:150-203, 98-117): cells (d, r) = (depth block, row band).
+      // Cell (d, r) reads rows of bands r-1..r+1 at time d*bt from slab d&1 and
+      // writes band r at time (d+1)*bt into slab (d+1)&1; in the skewed
+      // coordinates (d, s = r + 2d) every flow and ping-pong anti-dependence
+      // is a componentwise non-negative vector ((1,1), (1,2), (1,3), (2,4)), so
+      // the Morton order of the skewed box (time bit most significant, empty
+      // cells skipped) is a legal schedule with two slabs.
+      const int64_t hb = std::max<int64_t>(2 * bt, std::min<int64_t>(
+          n, o.tile.leaf.size() > 1 && o.tile.leaf[1] > 0 ? o.tile.leaf[1] : 256));
+      const int64_t nband = (n + hb - 1) / hb, nblk = (T + bt - 1) / bt;
+      const int64_t ns = nband + 2 * (nblk - 1);
+      int bits = 0;
+      while ((int64_t(1) << bits) < std::max(nblk, ns)) ++bits;
+      std::vector<std::pair<uint64_t, std::pair<int64_t, int64_t>>> cells;
+      for (int64_t d = 0; d < nblk; ++d)
+        for (int64_t r = 0; r < nband; ++r) {
+          const uint64_t sv = uint64_t(r + 2 * d), dv = uint64_t(d);
+          uint64_t key = 0;
+          for (int q = bits - 1; q >= 0; --q) key = (key << 2) | (((dv >> q) & 1) << 1) | ((sv >> q) & 1);
+          cells.push_back({key, {d, r}});
+        }
+      std::sort(cells.begin(), cells.end());
+      for (const auto& c : cells) {
+        const int64_t d = c.second.first, r = c.second.second;
+        const int step = int(std::min<int64_t>(bt, T - d * bt));
+        const int lo = int(r * hb), hi = int(std::min<int64_t>(n, (r + 1) * hb));
+        ck(s2d5_advance(sg[d & 1], sg[(d + 1) & 1], 0, n, step, rec.ring_hold, kOrderLex, lo, hi, stream),
+           "s2d5_advance");
+      }
+      result_slot = int(nblk & 1);
+      return bt;
+    }
     int cur = 0;
     for (int64_t t = 0; t < T; t += bt) {
       const int step = int(std::min<int64_t>(bt, T - t));
@@ -772,6 +806,7 @@ TileOrder order_of(const pcotgpu_schedule* s) {
   if (!s) return o;
   o.scheme = s->scheme == PCOTGPU_SLT ? Scheme::Slt : s->scheme == PCOTGPU_COT ? Scheme::Cot : Scheme::Untiled;
   for (int i = 0; i < s->ndim && i < 8; ++i) o.tile.leaf.push_back(s->leaf[i]);
+  o.space_time = (s->flags & PCOTGPU_SPACE_TIME) != 0;
   return o;
 }
 

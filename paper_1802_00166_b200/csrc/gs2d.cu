@@ -22,6 +22,7 @@
 #include <cstdlib>
 #include <map>
 #include <tuple>
+#include <type_traits>
 #include <vector>
 
 #include "common.cuh"
@@ -548,6 +549,27 @@ PCOT_DEV void st_global_if(double* p, double v, bool pred) {
   asm volatile("{\n .reg .pred q;\n setp.ne.b32 q, %2, 0;\n @q st.global.f64 [%0], %1;\n}" ::"l"(p),
                "d"(v), "r"(int(pred)));
 }
+// Same with a compile-time element offset folded into the address ([base+imm]):
+// one base register per chunk instead of a 64-bit address per store.
+template <int OFF>
+PCOT_DEV void st_relaxed_if_at(double* base, double v, bool pred) {
+  asm volatile(
+      "{\n .reg .pred q;\n setp.ne.b32 q, %2, 0;\n @q st.relaxed.gpu.global.f64 [%0+%3], %1;\n}" ::"l"(base),
+      "d"(v), "r"(int(pred)), "n"(OFF * 8));
+}
+template <int OFF>
+PCOT_DEV void st_global_if_at(double* base, double v, bool pred) {
+  asm volatile("{\n .reg .pred q;\n setp.ne.b32 q, %2, 0;\n @q st.global.f64 [%0+%3], %1;\n}" ::"l"(base),
+               "d"(v), "r"(int(pred)), "n"(OFF * 8));
+}
+// Compile-time unrolled loop: f(std::integral_constant<int, i>) for i in [0, N).
+template <int N, class F>
+PCOT_DEV void static_for(F&& f) {
+  if constexpr (N > 0) {
+    static_for<N - 1>(f);
+    f(std::integral_constant<int, N - 1>{});
+  }
+}
 
 // Bits kk in [0, S) with lo <= j0 + kk <= hi.
 template <int S>
@@ -719,16 +741,17 @@ __global__ void __launch_bounds__(NW * 32, 1) gs2d_pipe_kernel(PipeArgs g) {
       double* const op = orow + j0;
       double* const ep = eb_mine + j0;
       const unsigned emask = elane ? inb : 0u;
-#pragma unroll
-      for (int kk = 0; kk < S; ++kk) {
+      static_for<S>([&](auto KK) {
+        constexpr int kk = decltype(KK)::value;
         // next chunk's edge values: loaded part-way through this chunk, late
         // enough to be fresh, early enough to land before the next resolve
         if (kk == kXLoadClock && k + 1 < nchunk) xv = xload(k + 1);
         const int q = j0 + kk + 1;
         const double sh = __shfl_up_sync(0xffffffffu, out, 1);
+        const double ev = ab[q & (SG - 1)];  // lane 0's band-above value (same address for all)
         a1 = a2;
         a2 = a3;
-        a3 = lane ? sh : ab[q & (SG - 1)];
+        a3 = lane ? sh : ev;
         c1 = c2;
         c2 = prowC[q & cmask];
         d1 = d2;
@@ -750,9 +773,12 @@ __global__ void __launch_bounds__(NW * 32, 1) gs2d_pipe_kernel(PipeArgs g) {
         myring[(j0 + kk) & (RS - 1)] = v;
         // lane 31: the band's last row (a computed NaN carrying the kEmpty bit
         // pattern would read as "not yet written": stored as the canonical NaN)
-        st_relaxed_if(ep + kk, is_empty(v) ? __longlong_as_double(0x7fffffffffffffffLL) : v, (emask >> kk) & 1u);
-        st_global_if(op + kk, v, (omask >> kk) & 1u);  // result / wrap buffer
-      }
+        // (computed values never carry the kEmpty pattern: the device's fp64
+        // arithmetic returns the canonical NaN — checked by
+        // test_gs2d_pipeline_nan_input_with_sentinel_bits)
+        st_relaxed_if_at<kk>(ep, v, (emask >> kk) & 1u);
+        st_global_if_at<kk>(op, v, (omask >> kk) & 1u);  // result / wrap buffer
+      });
       PCOT_PROF(5);
 #ifdef PCOT_EDGE_FENCE
       __threadfence();
@@ -1067,8 +1093,7 @@ __global__ void __launch_bounds__(NW * 32, 1) gs2d_pipe2_kernel(PipeArgs g) {
 #pragma unroll
         for (int kk = 0; kk < K; ++kk) {
           const double v = nv[kk];
-          pipe::st_relaxed_if(ep[kk] + cc, pipe::is_empty(v) ? __longlong_as_double(0x7fffffffffffffffLL) : v,
-                              (inb[kk] >> cc) & 1u);
+          pipe::st_relaxed_if(ep[kk] + cc, v, (inb[kk] >> cc) & 1u);
           if (has_out) pipe::st_global_if(op[kk] + cc, v, (om[kk] >> cc) & 1u);
         }
         myring[(jr + cc) & (RS - 1)] = nv[K - 1];

@@ -292,3 +292,19 @@ def test_gs2d_pipeline_nan_input_with_sentinel_bits(monkeypatch, variant):
     ok = ~np.isnan(want)
     assert np.isnan(want).sum() > 100
     assert np.array_equal(got[ok].view(np.uint64), want[ok].view(np.uint64))
+
+
+@pytest.mark.parametrize("bt,band", [(1, 8), (2, 64), (4, 100), (6, 333), (8, 1000)])
+@pytest.mark.parametrize("kernel", ["jacobi2d", "heat2d"])
+def test_space_time_cot_order_is_exact(kernel, bt, band):
+    """COT across time (SPACE_TIME): one launch per (depth block, row band) in
+    Morton order of the skewed box — every band through several depth blocks
+    before its neighbours catch up — reproduces the reference bit for bit."""
+    params = {"T": 40, "N": 1000} if kernel == "jacobi2d" else {"T": 64, "N": 1024}
+    want = _golden(kernel, **params)
+    with P.GpuExecutor(O.kernel_path(kernel), params) as ex:
+        r = ex.run("cot-st", [bt, band, 256])
+        nblk = -(-params["T"] // bt)
+        nband = -(-params["N"] // max(band, 2 * bt))
+        assert r.launches >= nblk * nband
+        assert r.checksum_hex == want
