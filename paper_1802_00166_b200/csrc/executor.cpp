@@ -344,7 +344,7 @@ struct GpuExecutor::Impl {
       gs_plan = gs2d_plan_create(n, T, bt, bx, by, device);
       gs_cfg[0] = bt, gs_cfg[1] = bx, gs_cfg[2] = by;
     }
-    ck(copy_rows(gsa.p, gs_ld, in[0].p, in_ld, n, n, stream), "copy_rows");
+    ck(copy_rows_nosentinel(gsa.p, gs_ld, in[0].p, in_ld, n, n, stream), "copy_rows");
     ck(zero_ring_2d(gsa.p, gs_ld, n, stream), "zero_ring");
     ck(gs2d_run(gs_plan, gsa.p, gs_ld, stream), "gs2d_run");
     result_slot = 0;

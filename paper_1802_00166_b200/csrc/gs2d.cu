@@ -46,6 +46,7 @@ struct GsPlan {
   int64_t ebld = 0, ld = 0;
   double* wb[2] = {nullptr, nullptr};
   double* eb = nullptr;
+  int* gprog = nullptr;  // split-band progress words
   // fault word: a dependence wait that hit its spin cap (lost co-residency or
   // a scheduling bug) sets it; gs2d_run copies it to h_err after its launches
   int* d_err = nullptr;
@@ -468,6 +469,7 @@ struct PipeArgs {
   long long* prof;  // optional per-warp counters [nb * NW][16] (PCOTGPU_GS_PROF dev aid)
   int spin_ns;      // edge-poll backoff cap (ns)
   int* err;         // fault word (spin cap hit)
+  int* gprog;       // H > 1: per-CTA progress of its last warp, gpu scope [nb * H]
 };
 
 // CTA-scope acquire/release on the shared-memory progress words: the acquire
@@ -513,6 +515,24 @@ PCOT_DEV void wait_seen(const volatile int* p, int target, int& seen, int* err) 
   for (; !__all_sync(0xffffffffu, v >= target) && it < kSpinCap; ++it) {
     __nanosleep(8);
     v = vld(p);
+  }
+  if (it == kSpinCap) spin_fault(err);
+  seen = v;
+}
+
+// gpu-scope progress (split bands, H > 1): acquire loads by the whole warp.
+PCOT_DEV int ld_acquire_gpu(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+PCOT_DEV void wait_global(const int* p, int target, int& seen, int* err) {
+  if (seen >= target) return;
+  int v = ld_acquire_gpu(p);
+  long long it = 0;
+  for (; !__all_sync(0xffffffffu, v >= target) && it < kSpinCap; ++it) {
+    __nanosleep(64);
+    v = ld_acquire_gpu(p);
   }
   if (it == kSpinCap) spin_fault(err);
   seen = v;
@@ -579,8 +599,15 @@ PCOT_DEV unsigned span_mask(int j0, int lo, int hi) {
   return ((2u << khi) - 1u) & ~((1u << klo) - 1u);
 }
 
-template <int NW, int RS, int S>
-__global__ void __launch_bounds__(NW * 32, 1) gs2d_pipe_kernel(PipeArgs g) {
+// H > 1 splits a band over H CTAs (H x NW warps, level groups of NW levels
+// dealt round-robin: CTA h runs groups h, h+H, ...), so the band's work per
+// clock spreads over H SMs and the SMs of early and late bands of the
+// wavefront overlap; the group-to-group rows go through the wrap buffers (as
+// between passes), ordered by a gpu-scope progress word that an extra
+// publisher warp mirrors from the last warp's shared-memory progress (the
+// release fence stays off the compute warps).
+template <int NW, int RS, int S, int H = 1>
+__global__ void __launch_bounds__((NW + (H > 1)) * 32, H > 1 ? 2 : 1) gs2d_pipe_kernel(PipeArgs g) {
   static_assert(2 * S <= 32 && 3 * S + 4 <= IRS && S + 2 <= SG / 2, "chunk size");
   constexpr int RSP = RS + 1;  // odd lane pitch: ring accesses are bank-conflict free
   extern __shared__ __align__(16) double sm[];
@@ -589,11 +616,35 @@ __global__ void __launch_bounds__(NW * 32, 1) gs2d_pipe_kernel(PipeArgs g) {
   double* above = ir + 32 * IRS;                // [NW][SG] band b-1's last row, level t
   double* cabove = above + NW * SG;             // [NW][SG] same row, level t-1 (lane 0's C)
   volatile int* prog = reinterpret_cast<volatile int*>(cabove + NW * SG);  // [NW]
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, b = blockIdx.x;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int b = H > 1 ? int(blockIdx.x) / H : int(blockIdx.x);
+  const int h = H > 1 ? int(blockIdx.x) % H : 0;
   const int i0 = 1 + 32 * b;
   const bool has_above = b > 0;
-  if (lane == 0) prog[w] = 0;
+  if (lane == 0 && w < NW) prog[w] = 0;
   __syncthreads();
+  const int nclk_all = ((g.nclk + S - 1) / S) * S - 1;  // every warp's final published clock count
+  if constexpr (H > 1) {
+    if (w == NW) {  // publisher: mirror the last warp's progress to gpu scope
+      int* gp = g.gprog + blockIdx.x;
+      int last = 0;
+      for (int t = 1 + h * NW + NW - 1; t <= g.T; t += NW * H) {
+        const int done = t * BIG + nclk_all;
+        for (long long it = 0; last < done && it < kSpinCap; ++it) {
+          int v = vld(prog + NW - 1);
+          v = __shfl_sync(0xffffffffu, v, 0);
+          if (v >= last + 4 * S || v >= done) {  // every 4 chunks and at the level's end
+            __threadfence();  // the last warp's wrap-buffer rows before the progress
+            if (lane == 0) st_release(gp, v);
+            last = v;
+          } else {
+            __nanosleep(200);
+          }
+        }
+      }
+      return;
+    }
+  }
   double* myring = rb + (w * 32 + lane) * RSP;
   // edge-fetch roles: lanes [0, S) fetch a chunk's A columns (c+1) of band
   // b-1's last row at level t, lanes [S, 2S) the same columns at level t-1
@@ -612,7 +663,7 @@ __global__ void __launch_bounds__(NW * 32, 1) gs2d_pipe_kernel(PipeArgs g) {
   int seen_prod = 0, seen_cons = 0, seen_wrap = 0;  // progress words last observed
   long long t_first = 0, c_first = 0;  // globaltimer / clock64 at the first compute (prof)
   const long long t_entry = g.prof ? globaltimer() : 0;
-  for (int t = w + 1; t <= g.T; t += NW) {
+  for (int t = 1 + h * NW + w; t <= g.T; t += NW * H) {
     const int i = i0 - (t - 1) + lane;  // this lane's row at level t
     const bool row_ok = i >= 1 && i <= g.n - 2;
     // (selects, not g.wb[k]: a dynamic index into the parameter struct puts it
@@ -671,8 +722,14 @@ __global__ void __launch_bounds__(NW * 32, 1) gs2d_pipe_kernel(PipeArgs g) {
       if (p >= 0 && p < g.n) *reinterpret_cast<double2*>(irow + (p & (IRS - 1))) = v;
     };
     double2 pre[S / 2];  // warp 0: chunk k+1's new pairs, in flight during chunk k
+    // producer of warp 0's level t-1: this CTA's last warp (H = 1), or the
+    // previous group's CTA (gpu scope)
+    const int* gprod = H > 1 ? g.gprog + b * H + (h + H - 1) % H : nullptr;
     if (w == 0) {
-      if (t > 1) wait_smem(prog + NW - 1, plvl + need(S - 2 + 2), g.err);
+      if (t > 1) {
+        if (H > 1) wait_global(gprod, plvl + need(S - 2 + 2), seen_wrap, g.err);
+        else wait_smem(prog + NW - 1, plvl + need(S - 2 + 2), g.err);
+      }
       store_pair(0, 0, load_pair(0, 0));
 #pragma unroll
       for (int m = 1; m <= S / 2; ++m) pre[m - 1] = load_pair(0, m);
@@ -701,7 +758,10 @@ __global__ void __launch_bounds__(NW * 32, 1) gs2d_pipe_kernel(PipeArgs g) {
 #pragma unroll
         for (int m = 1; m <= S / 2; ++m) store_pair(k, m, pre[m - 1]);
         if (k + 1 < nchunk) {
-          if (t > 1) wait_seen(prog + NW - 1, plvl + need(c_hi + S + 2), seen_wrap, g.err);
+          if (t > 1) {
+            if (H > 1) wait_global(gprod, plvl + need(c_hi + S + 2), seen_wrap, g.err);
+            else wait_seen(prog + NW - 1, plvl + need(c_hi + S + 2), seen_wrap, g.err);
+          }
           PCOT_PROF(1);
 #pragma unroll
           for (int m = 1; m <= S / 2; ++m) pre[m - 1] = load_pair(k + 1, m);
@@ -720,8 +780,8 @@ __global__ void __launch_bounds__(NW * 32, 1) gs2d_pipe_kernel(PipeArgs g) {
         const int rel = c_hi + 1 - (RS - 4);
         if (rel > 0) {
           if (t + 1 <= g.T) wait_seen(prog + w + 1, clvl + need(rel), seen_cons, g.err);
-        } else if (t + 1 - NW >= 1) {
-          wait_seen(prog + w + 1, (t + 1 - NW) * BIG + fin, seen_cons, g.err);
+        } else if (t + 1 - NW * H >= 1) {  // the consumer's previous level in this CTA
+          wait_seen(prog + w + 1, (t + 1 - NW * H) * BIG + fin, seen_cons, g.err);
         }
       }
       PCOT_PROF(3);
@@ -773,8 +833,9 @@ __global__ void __launch_bounds__(NW * 32, 1) gs2d_pipe_kernel(PipeArgs g) {
         myring[(j0 + kk) & (RS - 1)] = v;
         // lane 31: the band's last row (a computed NaN carrying the kEmpty bit
         // pattern would read as "not yet written": stored as the canonical NaN)
-        // (computed values never carry the kEmpty pattern: the device's fp64
-        // arithmetic returns the canonical NaN — checked by
+        // (computed values never carry the kEmpty pattern: NaNs come only from
+        // input NaNs, whose payload the arithmetic propagates, and the copy-in
+        // maps the sentinel pattern to its neighbour NaN — copy_rows_nosentinel;
         // test_gs2d_pipeline_nan_input_with_sentinel_bits)
         st_relaxed_if_at<kk>(ep, v, (emask >> kk) & 1u);
         st_global_if_at<kk>(op, v, (omask >> kk) & 1u);  // result / wrap buffer
@@ -795,16 +856,16 @@ __global__ void __launch_bounds__(NW * 32, 1) gs2d_pipe_kernel(PipeArgs g) {
     __syncwarp();
   }
   if (g.prof && lane == 0)
-    for (int q = 0; q < 8; ++q) g.prof[(int64_t(b) * NW + w) * 16 + q] = pacc[q];
+    for (int q = 0; q < 8; ++q) g.prof[(int64_t(blockIdx.x) * NW + w) * 16 + q] = pacc[q];
   if (g.prof && lane == 0) {
-    g.prof[(int64_t(b) * NW + w) * 16 + 8] = t_first;
-    g.prof[(int64_t(b) * NW + w) * 16 + 9] = globaltimer();
-    g.prof[(int64_t(b) * NW + w) * 16 + 10] = c_first;
-    g.prof[(int64_t(b) * NW + w) * 16 + 11] = clock64();
-    g.prof[(int64_t(b) * NW + w) * 16 + 12] = t_entry;
+    g.prof[(int64_t(blockIdx.x) * NW + w) * 16 + 8] = t_first;
+    g.prof[(int64_t(blockIdx.x) * NW + w) * 16 + 9] = globaltimer();
+    g.prof[(int64_t(blockIdx.x) * NW + w) * 16 + 10] = c_first;
+    g.prof[(int64_t(blockIdx.x) * NW + w) * 16 + 11] = clock64();
+    g.prof[(int64_t(blockIdx.x) * NW + w) * 16 + 12] = t_entry;
     unsigned smid;
     asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
-    g.prof[(int64_t(b) * NW + w) * 16 + 13] = smid;
+    g.prof[(int64_t(blockIdx.x) * NW + w) * 16 + 13] = smid;
   }
 }
 
@@ -1247,6 +1308,7 @@ void gs2d_plan_destroy(GsPlan* p) {
   cudaFree(p->wb[0]);
   cudaFree(p->wb[1]);
   cudaFree(p->eb);
+  cudaFree(p->gprog);
   cudaFree(p->d_err);
   if (p->h_err) cudaFreeHost(p->h_err);
   delete p;
@@ -1257,6 +1319,8 @@ void gs2d_plan_destroy(GsPlan* p) {
 struct PipeVariant {
   int nw, rs, s, k;
   void (*kern)(pipe::PipeArgs);
+  int h = 1;  // CTAs per band (split bands)
+  int threads() const { return (nw + (h > 1 ? 1 : 0)) * 32; }
 };
 const PipeVariant kPipeVariants[] = {
     {16, 32, 8, 1, pipe::gs2d_pipe_kernel<16, 32, 8>},
@@ -1268,6 +1332,9 @@ const PipeVariant kPipeVariants[] = {
     {8, 64, 8, 2, pipe2::gs2d_pipe2_kernel<8, 2, 64, 8>},
     {8, 64, 8, 4, pipe2::gs2d_pipe2_kernel<8, 4, 64, 8>},
     {4, 64, 8, 4, pipe2::gs2d_pipe2_kernel<4, 4, 64, 8>},
+    {8, 32, 8, 1, pipe::gs2d_pipe_kernel<8, 32, 8, 2>, 2},    // 9: split bands, 2 x 8 warps
+    {8, 64, 8, 1, pipe::gs2d_pipe_kernel<8, 64, 8, 2>, 2},    // 10
+    {4, 64, 8, 1, pipe::gs2d_pipe_kernel<4, 64, 8, 2>, 2},    // 11: 2 x 4 warps
 };
 constexpr int kNumPipeVariants = sizeof(kPipeVariants) / sizeof(kPipeVariants[0]);
 const PipeVariant& pipe_variant() {
@@ -1303,9 +1370,9 @@ int64_t gs2d_pipe_segment(int64_t n, int64_t T, int device) {
   const size_t smem = gs2d_pipe_smem(v);
   int slots = 0;
   if (cudaSetDevice(device) != cudaSuccess ||
-      kernel_slots(reinterpret_cast<const void*>(v.kern), v.nw * 32, smem, &slots) != cudaSuccess)
+      kernel_slots(reinterpret_cast<const void*>(v.kern), v.threads(), smem, &slots) != cudaSuccess)
     return 0;
-  const int64_t cap = slots;
+  const int64_t cap = slots / v.h;  // bands that can be resident
   int64_t seg = std::min<int64_t>(T, 32 * cap - (n - 2) + 1);
   seg = std::min<int64_t>(seg, (int64_t(1) << 31) / pipe::BIG - 2);
   size_t free_b = 0, total_b = 0;
@@ -1333,9 +1400,12 @@ cudaError_t gs2d_pipe_run(GsPlan* p, double* a, int64_t ld, cudaStream_t stream)
       if ((e = cudaMalloc(&p->wb[q], size_t(p->n) * ld * 8)) != cudaSuccess) return e;
     if ((e = cudaMalloc(&p->eb, gs2d_pipe_edge_bytes(p->n, p->seg))) != cudaSuccess) return e;
   }
+  if (!p->gprog) {  // split-band progress words (H <= 4 CTAs per band)
+    if ((e = cudaMalloc(&p->gprog, size_t(p->nb + 1) * 4 * sizeof(int))) != cudaSuccess) return e;
+  }
   const PipeVariant& v = pipe_variant();
   const size_t smem = gs2d_pipe_smem(v);
-  if ((e = kernel_slots(reinterpret_cast<const void*>(v.kern), v.nw * 32, smem, nullptr)) != cudaSuccess)
+  if ((e = kernel_slots(reinterpret_cast<const void*>(v.kern), v.threads(), smem, nullptr)) != cudaSuccess)
     return e;
   for (int64_t t0 = 0; t0 < p->T; t0 += p->seg) {
     const int64_t len = std::min(p->seg, p->T - t0);
@@ -1353,7 +1423,9 @@ cudaError_t gs2d_pipe_launch(GsPlan* p, const PipeVariant& v, size_t smem, doubl
   // every edge slot back to kEmpty (written once per launch)
   if ((e = cudaMemsetAsync(p->eb, 0xff, gs2d_pipe_edge_bytes(p->n, len), stream)) != cudaSuccess)
     return e;
+  if ((e = cudaMemsetAsync(p->gprog, 0, size_t(nb) * v.h * sizeof(int), stream)) != cudaSuccess) return e;
   PipeArgs g;
+  g.gprog = p->gprog;
   g.a = a;
   g.wb[0] = p->wb[0];
   g.wb[1] = p->wb[1];
@@ -1368,7 +1440,7 @@ cudaError_t gs2d_pipe_launch(GsPlan* p, const PipeVariant& v, size_t smem, doubl
   g.err = p->d_err;
   g.spin_ns = env_int("PCOTGPU_GS_SPIN", 256);
   const char* pe = getenv("PCOTGPU_GS_PROF");  // development aid: cycle breakdown
-  const size_t np = size_t(nb) * v.nw * 16;
+  const size_t np = size_t(nb) * v.h * v.nw * 16;
   if (pe && atoi(pe)) {
     if ((e = cudaMalloc(&g.prof, np * 8)) != cudaSuccess) return e;
     cudaMemsetAsync(g.prof, 0, np * 8, stream);
@@ -1377,8 +1449,8 @@ cudaError_t gs2d_pipe_launch(GsPlan* p, const PipeVariant& v, size_t smem, doubl
   // cooperative launch makes that a launch-time guarantee — it fails with
   // cudaErrorCooperativeLaunchTooLarge instead of deadlocking.
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(nb);
-  cfg.blockDim = dim3(v.nw * 32);
+  cfg.gridDim = dim3(nb * v.h);
+  cfg.blockDim = dim3(v.threads());
   cfg.dynamicSmemBytes = smem;
   cfg.stream = stream;
   cudaLaunchAttribute attr[1];
@@ -1406,9 +1478,9 @@ cudaError_t gs2d_pipe_launch(GsPlan* p, const PipeVariant& v, size_t smem, doubl
       const int b = int(int64_t(nb - 1) * q / 4);
       double xw = 0, cw = 0, rw = 0;
       for (int w = 0; w < v.nw; ++w) {
-        xw += double(h[(size_t(b) * v.nw + w) * 16 + 0]);
-        cw += double(h[(size_t(b) * v.nw + w) * 16 + 5]);
-        rw += double(h[(size_t(b) * v.nw + w) * 16 + 2] + h[(size_t(b) * v.nw + w) * 16 + 3]);
+        xw += double(h[(size_t(b) * v.h * v.nw + w) * 16 + 0]);
+        cw += double(h[(size_t(b) * v.h * v.nw + w) * 16 + 5]);
+        rw += double(h[(size_t(b) * v.h * v.nw + w) * 16 + 2] + h[(size_t(b) * v.h * v.nw + w) * 16 + 3]);
       }
       fprintf(stderr, "  band %d: wait_xcta %.0f compute %.0f wait_intra %.0f (cyc/warp)\n", b,
               xw / v.nw, cw / v.nw, rw / v.nw);
@@ -1418,8 +1490,8 @@ cudaError_t gs2d_pipe_launch(GsPlan* p, const PipeVariant& v, size_t smem, doubl
       fprintf(stderr, "  timeline (us):");
       for (int q = 0; q <= 8; ++q) {
         const int b = int(int64_t(nb - 1) * q / 8);
-        fprintf(stderr, " b%d[%.1f,%.1f]", b, (h[(size_t(b) * v.nw) * 16 + 8] - t0) * 1e-3,
-                (h[(size_t(b) * v.nw + v.nw - 1) * 16 + 9] - t0) * 1e-3);
+        fprintf(stderr, " b%d[%.1f,%.1f]", b, (h[(size_t(b) * v.h * v.nw) * 16 + 8] - t0) * 1e-3,
+                (h[(size_t(b) * v.h * v.nw + v.nw - 1) * 16 + 9] - t0) * 1e-3);
       }
       long long emin = h[12], emax = h[12];
       int late = 0;
@@ -1438,7 +1510,7 @@ cudaError_t gs2d_pipe_launch(GsPlan* p, const PipeVariant& v, size_t smem, doubl
       for (int w = 0; w < v.nw; ++w) {
         fprintf(stderr, "  band %d warp %2d:", b, w);
         for (int m = 0; m < 8; ++m)
-          fprintf(stderr, " %s=%lld", names[m], h[(size_t(b) * v.nw + w) * 16 + m]);
+          fprintf(stderr, " %s=%lld", names[m], h[(size_t(b) * v.h * v.nw + w) * 16 + m]);
         fprintf(stderr, "\n");
       }
     }

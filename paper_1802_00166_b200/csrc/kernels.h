@@ -84,6 +84,10 @@ cudaError_t fill_init_value_3d(const Grid3D& g, uint64_t name_hash, cudaStream_t
 // plane r / rows_per_plane, row r % rows_per_plane (dense source).
 cudaError_t copy_rows(double* dst, int64_t ldd, const double* src, int64_t lds, int64_t nrows,
                       int64_t ncols, cudaStream_t stream, int64_t pd = 0, int64_t rows_per_plane = 0);
+// copy_rows (2-D, dense source) that maps the Gauss-Seidel edge-slot sentinel
+// bit pattern 0xffff...ffff to 0xffff...fffe (both NaN).
+cudaError_t copy_rows_nosentinel(double* dst, int64_t ldd, const double* src, int64_t lds, int64_t nrows,
+                                 int64_t ncols, cudaStream_t stream);
 // Zero (or keep) the ring of a 2-D grid: cells on rows 0/N-1, cols 0/N-1.
 cudaError_t zero_ring_2d(double* origin, int64_t ld, int64_t n, cudaStream_t stream);
 cudaError_t zero_ring_3d(const Grid3D& g, cudaStream_t stream);

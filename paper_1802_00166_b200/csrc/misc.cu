@@ -55,6 +55,24 @@ __global__ void copy_rows_kernel(double* dst, int64_t ldd, const double* src, in
   }
 }
 
+// Copy that maps the one bit pattern the Gauss-Seidel pipeline reserves as its
+// "not yet written" edge-slot sentinel (0xffff...ffff, a NaN) to its neighbour
+// NaN 0xffff...fffe.  The device's fp64 arithmetic propagates an input NaN's
+// payload (measured: without this an input cell holding the sentinel bits
+// stalled the band below), so with no such input no computed value can carry
+// it; any other input bit pattern is copied unchanged.
+__global__ void copy_rows_nosentinel_kernel(double* dst, int64_t ldd, const double* src, int64_t lds,
+                                            int64_t nrows, int64_t ncols) {
+  const int64_t total = nrows * ncols;
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < total;
+       e += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t r = e / ncols, c = e - r * ncols;
+    long long v = __double_as_longlong(src[r * lds + c]);
+    if (v == -1LL) v = -2LL;
+    dst[r * ldd + c] = __longlong_as_double(v);
+  }
+}
+
 __global__ void zero_ring2d_kernel(double* o, int64_t ld, int64_t n) {
   for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < 4 * n;
        e += int64_t(gridDim.x) * blockDim.x) {
@@ -111,6 +129,14 @@ cudaError_t copy_rows(double* dst, int64_t ldd, const double* src, int64_t lds, 
   if (nrows <= 0 || ncols <= 0) return cudaSuccess;
   copy_rows_kernel<<<grid_for(nrows * ncols), 256, 0, stream>>>(dst, ldd, src, lds, nrows, ncols,
                                                                 pd, rpp);
+  count_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t copy_rows_nosentinel(double* dst, int64_t ldd, const double* src, int64_t lds, int64_t nrows,
+                                 int64_t ncols, cudaStream_t stream) {
+  if (nrows <= 0 || ncols <= 0) return cudaSuccess;
+  copy_rows_nosentinel_kernel<<<grid_for(nrows * ncols), 256, 0, stream>>>(dst, ldd, src, lds, nrows, ncols);
   count_launch();
   return cudaGetLastError();
 }

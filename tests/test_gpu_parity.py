@@ -73,7 +73,7 @@ def test_gs2d_tile_shapes(tile):
 GS_PIPE_SHAPES = [(1, 3), (1, 34), (2, 35), (13, 66), (12, 97), (25, 100), (40, 130), (7, 1000)]
 
 
-@pytest.mark.parametrize("variant", [0, 1, 2, 5, 6, 7, 8])
+@pytest.mark.parametrize("variant", [0, 1, 2, 5, 6, 7, 8, 9, 11])
 @pytest.mark.parametrize("T,N", GS_PIPE_SHAPES)
 def test_gs2d_pipeline_matches_oracle(monkeypatch, variant, T, N):
     """Systolic pipeline (untiled default): every variant (warps per band x ring
@@ -100,7 +100,7 @@ def test_gs2d_pipeline_multi_launch_segments():
     assert np.array_equal(got.view(np.uint64), want.view(np.uint64))
 
 
-@pytest.mark.parametrize("variant", [0, 1, 2, 5, 6, 7, 8])
+@pytest.mark.parametrize("variant", [0, 1, 2, 5, 6, 7, 8, 9, 11])
 @pytest.mark.parametrize("T,N", [(16, 1024), (64, 4096)])
 def test_gs2d_pipeline_goldens_repeated(monkeypatch, variant, T, N):
     """Reference checksums, three runs in a row on one executor (edge slots
@@ -274,7 +274,7 @@ def test_run_batch_errors():
         assert np.array_equal(one, ex.array_data("Out"))
 
 
-@pytest.mark.parametrize("variant", [0, 5, 7])
+@pytest.mark.parametrize("variant", [0, 5, 7, 9])
 def test_gs2d_pipeline_nan_input_with_sentinel_bits(monkeypatch, variant):
     """An input NaN carrying the edge slots' "not yet written" bit pattern
     (0xffff...ffff) must neither stall the pipeline nor leak: the run returns,
@@ -283,6 +283,7 @@ def test_gs2d_pipeline_nan_input_with_sentinel_bits(monkeypatch, variant):
     N, T = 200, 9
     F = O.init_array("F", N * N)
     F.view(np.uint64)[57 * N + 101] = np.uint64(0xFFFFFFFFFFFFFFFF)
+    F.view(np.uint64)[120 * N + 33] = np.uint64(0x7FF8000000000123)  # a NaN with another payload
     want = O.gs2d9(N, T, F)
     with P.GpuExecutor("gs2d", {"T": T, "N": N}) as ex:
         ex.write_array("F", F)
