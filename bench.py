@@ -586,9 +586,11 @@ def measure_e2e(args, P, torch, dist, S, dev, world, rows, updates, local):
     import numpy as np
 
     n_cells = rows * args.cols
-    # host copy of this rank's F, produced by the device generator once (untimed)
+    # host copy of this rank's F, produced by the device generator once (untimed);
+    # with several ranks on one host the output lands in a second pinned buffer
+    # only at N=1 (8 ranks x 2 x 8 GiB pinned would be 128 GiB of host memory)
     host_F = torch.empty(n_cells, dtype=torch.float64, pin_memory=True)
-    host_out = torch.empty(n_cells, dtype=torch.float64, pin_memory=True)
+    host_out = torch.empty(n_cells, dtype=torch.float64, pin_memory=True) if world == 1 else host_F
     stream = torch.cuda.current_stream(dev)
     if world == 1 and rows == args.cols:
         # pcotgpu_run_batch: each step's F goes in and its Out comes back through
@@ -643,7 +645,8 @@ def measure_e2e(args, P, torch, dist, S, dev, world, rows, updates, local):
     return {"value": updates / (ms / 1e3) / 1e9, "unit": "GUpdates/s",
             "h2d_bytes_per_step": n_cells * 8, "d2h_bytes_per_step": n_cells * 8,
             "ms_per_step": ms, "steps": steps,
-            "path": "pinned host slab copies + sharded run"}
+            "path": "pinned host slab copies + sharded run (per rank: the slab in, the result "
+                    "back into the same pinned buffer)"}
 
 
 if __name__ == "__main__":

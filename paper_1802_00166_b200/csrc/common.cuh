@@ -98,6 +98,33 @@ PCOT_DEV void st_release(int* p, int v) {
 
 PCOT_DEV double ld_cg(const double* p) { return __ldcg(p); }
 
+// ---------------------------------------------------------------- compact Morton (COT) order
+// The id-th point, in Morton (Z) order, of the W x H rectangle (x fast bit):
+// descends the quadtree of the power-of-two cover, skipping children by the
+// number of rectangle points they hold, so a launch of exactly W*H CTAs walks
+// the recursive order with no idle CTAs (children in the reference's
+// split_orthants bit order, tiler.cpp:98-117).
+__host__ __device__ __forceinline__ void morton_compact(int id, int W, int H, int& x, int& y) {
+  int side = 1;
+  while (side < W || side < H) side <<= 1;
+  int x0 = 0, y0 = 0;
+  for (int s = side >> 1; s >= 1; s >>= 1) {
+    for (int c = 0; c < 4; ++c) {
+      const int cx = c & 1, cy = c >> 1;
+      const int ox = W - (x0 + cx * s), oy = H - (y0 + cy * s);
+      const int cnt = (ox <= 0 || oy <= 0) ? 0 : (ox < s ? ox : s) * (oy < s ? oy : s);
+      if (id < cnt) {
+        x0 += cx * s;
+        y0 += cy * s;
+        break;
+      }
+      id -= cnt;
+    }
+  }
+  x = x0;
+  y = y0;
+}
+
 // Device-wide nanosecond timer (profiling aids).
 PCOT_DEV long long globaltimer() {
   long long t;

@@ -65,14 +65,7 @@ __global__ void __launch_bounds__(G::NTHR, 1)
     tm = blockIdx.x / tiles_n;
     tn = blockIdx.x - tm * tiles_n;
   } else {
-    int x = 0, y = 0;
-    for (int b = 0; b < 12; ++b) {
-      x |= ((blockIdx.x >> (2 * b)) & 1) << b;
-      y |= ((blockIdx.x >> (2 * b + 1)) & 1) << b;
-    }
-    tm = y;
-    tn = x;
-    if (tm >= tiles_m || tn >= tiles_n) return;
+    morton_compact(int(blockIdx.x), tiles_n, tiles_m, tn, tm);
   }
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int wm = warp / G::WN, wn = warp % G::WN;
@@ -191,12 +184,7 @@ cudaError_t dgemm_nn(const double* A, const double* B, double* C, int64_t n, int
       (reinterpret_cast<uintptr_t>(C) & 15))
     return cudaErrorInvalidValue;
   const int tiles_m = int((n + BM - 1) / BM), tiles_n = int((n + BN - 1) / BN);
-  int grid = tiles_m * tiles_n;
-  if (order == kOrderMorton) {
-    int side = 1;
-    while (side < tiles_m || side < tiles_n) side <<= 1;
-    grid = side * side;
-  }
+  const int grid = tiles_m * tiles_n;  // both orders (compact Morton rank for COT)
   const int variant = env_int("PCOTGPU_DGEMM_VARIANT", 0);  // 0: default
   // measured on the B200 at N=4096 (tools/kbench.py gemm; profiles/dgemm_r01.md)
   switch (variant) {

@@ -59,22 +59,17 @@ struct S2Args {
   int64_t mir_lo, mir_hi;
 };
 
-// Tile id -> (strip, chunk): lexicographic (SLT-like) or Morton/Z order over a
-// power-of-two cover (the COT recursive order, reference tiler.cpp:150-203).
+// Tile id -> (strip, chunk): lexicographic (SLT-like) or Morton/Z order of the
+// strips x chunks rectangle (the COT recursive order, reference
+// tiler.cpp:150-203), ranked compactly: no idle CTAs.
 PCOT_DEV bool tile_coords(int id, int nstrips, int nchunks, int order, int& strip, int& chunk) {
   if (order == kOrderLex) {
     chunk = id / nstrips;
     strip = id - chunk * nstrips;
     return true;
   }
-  int x = 0, y = 0;
-  for (int b = 0; b < 16; ++b) {
-    x |= ((id >> (2 * b)) & 1) << b;
-    y |= ((id >> (2 * b + 1)) & 1) << b;
-  }
-  chunk = y;
-  strip = x;
-  return strip < nstrips && chunk < nchunks;
+  morton_compact(id, nstrips, nchunks, strip, chunk);
+  return true;
 }
 
 __host__ __device__ constexpr int smod3(int v) { return ((v % 3) + 3) % 3; }
@@ -429,14 +424,7 @@ cudaError_t launch_cfg(S2Args a, int ring_hold, int rows, cudaStream_t stream) {
     a.nchunks = force_chunks;
     a.H = (rows + force_chunks - 1) / force_chunks;
   }
-  int grid;
-  if (a.order == kOrderMorton) {
-    int side = 1;
-    while (side < a.nstrips || side < a.nchunks) side <<= 1;
-    grid = side * side;
-  } else {
-    grid = a.nstrips * a.nchunks;
-  }
+  const int grid = a.nstrips * a.nchunks;  // both orders (compact Morton rank for COT)
   if (env_int("PCOTGPU_S2D5_DEBUG", 0))
     std::fprintf(stderr, "s2d5 bt=%d C=%d NT=%d slots=%d strips=%d chunks=%d H=%d grid=%d\n", BT, C,
                  NT, sl, a.nstrips, a.nchunks, a.H, grid);

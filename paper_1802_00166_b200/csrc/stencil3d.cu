@@ -260,18 +260,8 @@ __global__ void __launch_bounds__(G::NT, G::MINB) s3d7_kernel(S3Args a) {
   if (a.order == kOrderLex) {
     tj = tile / a.nk;
     tk = tile - tj * a.nk;
-  } else {  // Morton over (tk, tj)
-    int side = 1;
-    while (side < a.nk || side < a.nj) side <<= 1;
-    int x = 0, y = 0, id = blockIdx.x % (side * side);
-    chunk = blockIdx.x / (side * side);
-    for (int b = 0; b < 12; ++b) {
-      x |= ((id >> (2 * b)) & 1) << b;
-      y |= ((id >> (2 * b + 1)) & 1) << b;
-    }
-    tk = x;
-    tj = y;
-    if (tk >= a.nk || tj >= a.nj) return;
+  } else {  // Morton over (tk, tj), compact rank
+    morton_compact(tile, a.nk, a.nj, tk, tj);
   }
   if (threadIdx.x == 0) {
     for (int i = 0; i < G::PF; ++i) mbar_init(&bars[i], 1);
@@ -315,14 +305,7 @@ cudaError_t launch3(S3Args a, cudaStream_t stream) {
     a.nchunks = fc;
     a.H = (a.n + fc - 1) / fc;
   }
-  int grid;
-  if (a.order == kOrderLex) {
-    grid = a.nk * a.nj * a.nchunks;
-  } else {
-    int side = 1;
-    while (side < a.nk || side < a.nj) side <<= 1;
-    grid = side * side * a.nchunks;
-  }
+  const int grid = a.nk * a.nj * a.nchunks;  // both orders
   fn<<<grid, G::NT, smem, stream>>>(a);
   count_launch();
   return cudaGetLastError();
@@ -675,18 +658,8 @@ __global__ void __launch_bounds__(G::NT, G::MINB)
   if (a.order == kOrderLex) {
     tj = tile / a.nk;
     tk = tile - tj * a.nk;
-  } else {  // Morton over (tk, tj)
-    int side = 1;
-    while (side < a.nk || side < a.nj) side <<= 1;
-    int x = 0, y = 0, id = blockIdx.x % (side * side);
-    chunk = blockIdx.x / (side * side);
-    for (int b = 0; b < 12; ++b) {
-      x |= ((id >> (2 * b)) & 1) << b;
-      y |= ((id >> (2 * b + 1)) & 1) << b;
-    }
-    tk = x;
-    tj = y;
-    if (tk >= a.nk || tj >= a.nj) return;
+  } else {  // Morton over (tk, tj), compact rank
+    morton_compact(tile, a.nk, a.nj, tk, tj);
   }
   if (threadIdx.x == 0) {
     for (int i = 0; i < G::PF; ++i) mbar_init(&bars[i], 1);
@@ -754,14 +727,7 @@ cudaError_t launch3v2(S3Args a, cudaStream_t stream) {
     a.nchunks = fc;
     a.H = (a.n + fc - 1) / fc;
   }
-  int grid;
-  if (a.order == kOrderLex) {
-    grid = a.nk * a.nj * a.nchunks;
-  } else {
-    int side = 1;
-    while (side < a.nk || side < a.nj) side <<= 1;
-    grid = side * side * a.nchunks;
-  }
+  const int grid = a.nk * a.nj * a.nchunks;  // both orders
   CUtensorMap tmap;
   cudaError_t e = encode_plane_map(&tmap, a, G::KL, G::JL);
   if (e != cudaSuccess) return e;
