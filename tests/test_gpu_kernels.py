@@ -222,3 +222,39 @@ def test_sharded_p2p_mode_runs_through_symmetric_memory():
     p = subprocess.run([sys.executable, "-c", code], cwd=O.REPO, capture_output=True, text=True,
                        timeout=600)
     assert p.returncode == 0 and "ok" in p.stdout, p.stdout + p.stderr
+
+
+def test_executors_on_concurrent_host_threads():
+    """Distinct executors may run concurrently (reference sweep.cpp:82-128 runs one
+    Executor per worker thread): four host threads, each with its own executor and
+    kernel family, first launches racing on the per-(kernel, device) launch caches
+    (kernel_slots) — every result equals the reference golden."""
+    import threading
+
+    from tests import oracle_ctypes as O
+
+    cases = [("jacobi2d", {"T": 40, "N": 1000}), ("heat3d_b", {"T": 20, "N": 130}),
+             ("gs2d", {"T": 16, "N": 1024}), ("jacobi2d", {"T": 64, "N": 1024})]
+    want = {}
+    for k, p in cases:
+        want[(k, str(p))] = [e["checksum"] for e in O.goldens() if e["kernel"] == k and e["params"] == p][0]
+    got, errors = {}, []
+    start = threading.Barrier(len(cases))
+
+    def work(k, p):
+        try:
+            with P.GpuExecutor(k, p) as ex:
+                start.wait()
+                for _ in range(3):
+                    got.setdefault((k, str(p)), set()).add(ex.run("cot", None).checksum_hex)
+        except Exception as e:  # surfaced below
+            errors.append(repr(e))
+
+    th = [threading.Thread(target=work, args=c) for c in cases]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=300)
+    assert not errors, errors
+    for key, w in want.items():
+        assert got[key] == {w}, key
