@@ -470,6 +470,7 @@ struct PipeArgs {
   int spin_ns;      // edge-poll backoff cap (ns)
   int* err;         // fault word (spin cap hit)
   int* gprog;       // H > 1: per-CTA progress of its last warp, gpu scope [nb * H]
+  int wait_ns;      // sleep per poll of a warp-to-warp progress wait
 };
 
 // CTA-scope acquire/release on the shared-memory progress words: the acquire
@@ -499,21 +500,21 @@ PCOT_DEV void spin_fault(int* err) {
 // Waits are executed by the whole warp (every lane reads the same word, one
 // transaction) and exit on a warp vote: a lane-0-only spin leaves the warp
 // diverged and every later shuffle takes the compiler's slow collective path.
-PCOT_DEV void wait_smem(const volatile int* p, int target, int* err) {
+PCOT_DEV void wait_smem(const volatile int* p, int target, int* err, int ns = 8) {
   long long it = 0;
-  for (; !__all_sync(0xffffffffu, vld(p) >= target) && it < kSpinCap; ++it) __nanosleep(8);
+  for (; !__all_sync(0xffffffffu, vld(p) >= target) && it < kSpinCap; ++it) __nanosleep(ns);
   if (it == kSpinCap) spin_fault(err);
 }
 
 // Same wait through a per-warp cache of the last value seen: progress words
 // only grow, and an earlier acquire of a value >= target already orders the
 // reads that need it, so a producer running ahead costs no shared load.
-PCOT_DEV void wait_seen(const volatile int* p, int target, int& seen, int* err) {
+PCOT_DEV void wait_seen(const volatile int* p, int target, int& seen, int* err, int ns = 8) {
   if (seen >= target) return;
   int v = vld(p);
   long long it = 0;
   for (; !__all_sync(0xffffffffu, v >= target) && it < kSpinCap; ++it) {
-    __nanosleep(8);
+    __nanosleep(ns);
     v = vld(p);
   }
   if (it == kSpinCap) spin_fault(err);
@@ -728,7 +729,7 @@ __global__ void __launch_bounds__((NW + (H > 1)) * 32, H > 1 ? 2 : 1) gs2d_pipe_
     if (w == 0) {
       if (t > 1) {
         if (H > 1) wait_global(gprod, plvl + need(S - 2 + 2), seen_wrap, g.err);
-        else wait_smem(prog + NW - 1, plvl + need(S - 2 + 2), g.err);
+        else wait_smem(prog + NW - 1, plvl + need(S - 2 + 2), g.err, g.wait_ns);
       }
       store_pair(0, 0, load_pair(0, 0));
 #pragma unroll
@@ -760,7 +761,7 @@ __global__ void __launch_bounds__((NW + (H > 1)) * 32, H > 1 ? 2 : 1) gs2d_pipe_
         if (k + 1 < nchunk) {
           if (t > 1) {
             if (H > 1) wait_global(gprod, plvl + need(c_hi + S + 2), seen_wrap, g.err);
-            else wait_seen(prog + NW - 1, plvl + need(c_hi + S + 2), seen_wrap, g.err);
+            else wait_seen(prog + NW - 1, plvl + need(c_hi + S + 2), seen_wrap, g.err, g.wait_ns);
           }
           PCOT_PROF(1);
 #pragma unroll
@@ -770,7 +771,7 @@ __global__ void __launch_bounds__((NW + (H > 1)) * 32, H > 1 ? 2 : 1) gs2d_pipe_
       PCOT_PROF(7);
       // producer ahead: D of clock c is producer lane l's column j+1, computed
       // at the producer's clock c+1
-      if (w > 0) wait_seen(prog + w - 1, plvl + need(c_hi + 2), seen_prod, g.err);
+      if (w > 0) wait_seen(prog + w - 1, plvl + need(c_hi + 2), seen_prod, g.err, g.wait_ns);
       PCOT_PROF(2);
       if (w < NW - 1) {
         // ring reuse: the consumer (level t+1) must have read what this chunk
@@ -779,9 +780,9 @@ __global__ void __launch_bounds__((NW + (H > 1)) * 32, H > 1 ? 2 : 1) gs2d_pipe_
         // t+1, since every slot is written, out-of-range columns included.
         const int rel = c_hi + 1 - (RS - 4);
         if (rel > 0) {
-          if (t + 1 <= g.T) wait_seen(prog + w + 1, clvl + need(rel), seen_cons, g.err);
+          if (t + 1 <= g.T) wait_seen(prog + w + 1, clvl + need(rel), seen_cons, g.err, g.wait_ns);
         } else if (t + 1 - NW * H >= 1) {  // the consumer's previous level in this CTA
-          wait_seen(prog + w + 1, (t + 1 - NW * H) * BIG + fin, seen_cons, g.err);
+          wait_seen(prog + w + 1, (t + 1 - NW * H) * BIG + fin, seen_cons, g.err, g.wait_ns);
         }
       }
       PCOT_PROF(3);
@@ -1439,6 +1440,7 @@ cudaError_t gs2d_pipe_launch(GsPlan* p, const PipeVariant& v, size_t smem, doubl
   g.prof = nullptr;
   g.err = p->d_err;
   g.spin_ns = env_int("PCOTGPU_GS_SPIN", 256);
+  g.wait_ns = env_int("PCOTGPU_GS_WAIT", 8);
   const char* pe = getenv("PCOTGPU_GS_PROF");  // development aid: cycle breakdown
   const size_t np = size_t(nb) * v.h * v.nw * 16;
   if (pe && atoi(pe)) {
