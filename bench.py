@@ -275,6 +275,18 @@ def dmma_peak():
         return 40.0, "fallback (nominal B200 FP64 tensor)"
 
 
+def dadd_latency():
+    """Measured dependent-DADD latency in cycles (tools/fp64_peaks.cu)."""
+    try:
+        with open(os.path.join(REPO, "profiles", "fp64_peaks_r01.json")) as f:
+            for r in json.load(f)["results"]:
+                if r["probe"] == "dadd_latency_cycles":
+                    return float(r["value"])
+    except (OSError, ValueError, KeyError):
+        pass
+    return 8.4
+
+
 def golden_checksum(kernel, params):
     try:
         with open(os.path.join(REPO, "tests", "golden", "golden.json")) as f:
@@ -319,9 +331,8 @@ def per_config(P, torch, dev, local, hbm_peak, reps_ms=1000.0):
     for tag, kernel, params, sample, init, sample_work in PER_CONFIG:
         with P.GpuExecutor(kernel, params, device=local) as ex:
             first = ex.run_untiled(skip_checksum=(kernel == "gemm"))
-            for _ in range(3):
-                ex.run_untiled(skip_checksum=True)
-            reps = int(max(5, min(200, reps_ms / max(first.device_ms, 1e-3))))
+            warm = [ex.run_untiled(skip_checksum=True).device_ms for _ in range(3)]
+            reps = int(max(5, min(200, reps_ms / max(min(warm), 1e-3))))
             times = []
             with ClockSampler(local) as clocks:
                 for _ in range(reps):
@@ -348,12 +359,23 @@ def per_config(P, torch, dev, local, hbm_peak, reps_ms=1000.0):
                 e["GUpd/s"] = round(gu, 1)
                 if kernel == "gs2d":
                     # in place: the grid crosses HBM once per launch of `seg` sweeps;
-                    # the bound is the update's dependence chain, not bytes
+                    # the bound is the update's dependence chain, not bytes.  The
+                    # wavefront h = 4t + 2i + j orders every point after all of its
+                    # inputs: 4(T-1) + 3(N-3) + 1 dependent steps, each at least one
+                    # update's serial latency (9 chained fp64 ops after the previous
+                    # point's result + the div-by-9: 11 x the measured DADD latency)
                     fl = 11.0  # 8 DADD + div-by-9 (DMUL + 2 DFMA)
                     dadd_peak = 18.4e12  # measured DADD issue (profiles/fp64_peaks_r01.json)
+                    T_, N_ = params["T"], params["N"]
+                    steps = 4 * (T_ - 1) + 3 * (N_ - 3) + 1
+                    lat = dadd_latency()
                     e["roofline"] = {"bound": "fp64 dependence chain (in-place wavefront)",
                                      "fp64_ops_per_update": fl,
                                      "fp64_issue_frac": round(gu * 1e9 * fl / dadd_peak, 3),
+                                     "critical_path_steps": steps,
+                                     "step_latency_cycles": round(fl * lat, 1),
+                                     "latency_bound_ms_at_max_clock": round(steps * fl * lat / 1965e3, 4),
+                                     "latency_frac": round(steps * fl * lat / 1965e3 / ms, 3),
                                      "launches_per_run": int(first.launches)}
                 else:
                     bpu = 16.0 / first.bt

@@ -78,6 +78,8 @@ class GpuExecutor {
 
   // beyond the reference API
   const Recognized& recognized() const;
+  // device interpreter only: last run's schedule, compiled (emitter) or not, build status
+  void generic_info(int* mode, int* compiled, std::string* why) const;
   void write_array(const std::string& array, const double* host, size_t n);
   void read_array(const std::string& array, double* host, size_t n) const;
   double* device_view(const std::string& array, int64_t* ld);

@@ -113,6 +113,17 @@ int pcotgpu_find_kernel_file(const char* name_or_path, char* out, size_t cap);
 int pcotgpu_check_maps(const char* kernel_json, const int64_t* params, size_t nparams,
                        const pcotgpu_map* maps, size_t nmaps, int* hot_path, char* why, size_t cap);
 
+/* Host only: the PRDG -> CUDA emitter's source for a kernel (the device
+ * interpreter's compiled form), written to `buf` (needs
+ * `*need` bytes incl. the NUL); with compile != 0 it is also compiled by NVRTC
+ * for sm_100a and `buf` receives the compiler log instead on failure. */
+int pcotgpu_generic_source(const char* kernel_json, const int64_t* params, size_t nparams, int compile,
+                           char* buf, size_t cap, size_t* need);
+/* After a run on the device interpreter: its schedule (0 sequential, 1 dataflow
+ * over ready flags, 2 dataflow over storage shadows) and whether the emitter's
+ * compiled kernels ran (else the interpreter); `why` gets the build status. */
+int pcotgpu_generic_info(const pcotgpu_handle* h, int* mode, int* compiled, char* why, size_t cap);
+
 /* ---- Executor ------------------------------------------------------------ */
 /* Executor(p, params, maps) — exec.hpp:64.  Allocates device storage and
  * initialises inputs with init_value (exec.cpp:21-28, 281-294). */

@@ -13,7 +13,7 @@ import numpy as np
 
 __all__ = [
     "lib", "PcotError", "KernelInfo", "ExecResult", "GpuExecutor", "recognize",
-    "find_kernel_file", "load_kernel_text", "fnv1a", "FAMILIES", "SCHEMES", "check_maps",
+    "find_kernel_file", "load_kernel_text", "fnv1a", "FAMILIES", "SCHEMES", "check_maps", "generic_source",
 ]
 
 PKG = os.path.dirname(os.path.abspath(__file__))
@@ -90,6 +90,10 @@ _SIGS = [
     ("pcotgpu_check_maps", ctypes.c_int, [ctypes.c_char_p, _I64P, ctypes.c_size_t, ctypes.POINTER(MapC),
                                           ctypes.c_size_t, ctypes.POINTER(ctypes.c_int), ctypes.c_char_p,
                                           ctypes.c_size_t]),
+    ("pcotgpu_generic_source", ctypes.c_int, [ctypes.c_char_p, _I64P, ctypes.c_size_t, ctypes.c_int,
+                                              ctypes.c_char_p, ctypes.c_size_t, ctypes.POINTER(ctypes.c_size_t)]),
+    ("pcotgpu_generic_info", ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(ctypes.c_int),
+                                            ctypes.POINTER(ctypes.c_int), ctypes.c_char_p, ctypes.c_size_t]),
     ("pcotgpu_run", ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(Schedule), ctypes.POINTER(ExecResult)]),
     ("pcotgpu_run_untiled", ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(ExecResult)]),
     ("pcotgpu_run_batch", ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(Schedule), ctypes.c_size_t,
@@ -219,6 +223,22 @@ def check_maps(kernel, params, maps):
     why = ctypes.create_string_buffer(512)
     _check(lib().pcotgpu_check_maps(text.encode(), arr, n, marr, len(maps), ctypes.byref(hot), why, 512))
     return bool(hot.value), why.value.decode()
+
+
+def generic_source(kernel, params, compile=False):
+    """Host only: the PRDG -> CUDA emitter's source for a kernel; compile=True
+    also compiles it with NVRTC for sm_100a (PcotError Unsupported with the
+    compiler log on failure)."""
+    text = load_kernel_text(kernel)
+    arr, n = _params_array(text, params)
+    need = ctypes.c_size_t()
+    lib().pcotgpu_generic_source(text.encode(), arr, n, 0, None, 0, ctypes.byref(need))
+    buf = ctypes.create_string_buffer(max(need.value, 1) + 65536)
+    st = lib().pcotgpu_generic_source(text.encode(), arr, n, int(bool(compile)), buf, len(buf), ctypes.byref(need))
+    if st != 0:
+        raise PcotError(ERROR_KINDS.get(st, "status %d" % st),
+                        lib().pcotgpu_last_error().decode(errors="replace") + "\n" + buf.value.decode(errors="replace"))
+    return buf.value.decode()
 
 
 def recognize(kernel, params):
@@ -363,6 +383,13 @@ class GpuExecutor:
         ld = ctypes.c_int64()
         _check(lib().pcotgpu_device_view(self._h, name.encode(), ctypes.byref(p), ctypes.byref(ld)))
         return p.value, ld.value
+
+    def generic_info(self):
+        """Device interpreter only: (schedule mode, compiled by the emitter, status)."""
+        mode, comp = ctypes.c_int(), ctypes.c_int()
+        why = ctypes.create_string_buffer(4096)
+        _check(lib().pcotgpu_generic_info(self._h, ctypes.byref(mode), ctypes.byref(comp), why, 4096))
+        return mode.value, bool(comp.value), why.value.decode(errors="replace")
 
     def set_stream(self, stream_ptr):
         _check(lib().pcotgpu_set_stream(self._h, ctypes.c_void_p(stream_ptr)))

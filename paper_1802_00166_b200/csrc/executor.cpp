@@ -709,6 +709,12 @@ uint64_t GpuExecutor::array_base(const std::string& a) const {
   fail(ErrorKind::Validation, "array_base: unknown array " + a);
 }
 const Recognized& GpuExecutor::recognized() const { return impl_->rec; }
+void GpuExecutor::generic_info(int* mode, int* compiled, std::string* why) const {
+  if (!impl_->generic) fail(ErrorKind::Unsupported, "generic_info: this kernel runs on a hand-written kernel");
+  if (mode) *mode = impl_->gcounts.mode;
+  if (compiled) *compiled = impl_->gcounts.compiled ? 1 : 0;
+  if (why) *why = generic_jit_status(impl_->gplan);
+}
 void GpuExecutor::write_array(const std::string& a, const double* host, size_t n) {
   int q = impl_->input_slot(a);
   if (q < 0) fail(ErrorKind::Validation, "write_array: " + a + " is not an input");
@@ -973,6 +979,46 @@ int pcotgpu_array_base(const pcotgpu_handle* h, const char* array, uint64_t* bas
 
 int pcotgpu_array_words(const pcotgpu_handle* h, const char* array, uint64_t* words) {
   return guarded([&] { *words = h->ex->array_words(array); });
+}
+
+int pcotgpu_generic_source(const char* kernel_json, const int64_t* params, size_t nparams, int compile,
+                           char* buf, size_t cap, size_t* need) {
+  return guarded([&] {
+    if (!kernel_json) fail(ErrorKind::Validation, "null argument");
+    KernelSpec k = parse_kernel(kernel_json);
+    std::unique_ptr<GenericPlan, void (*)(GenericPlan*)> plan(
+        generic_plan_create(k, IntVec(params, params + nparams), {}, 0, true), generic_plan_destroy);
+    std::string text = generic_emit_source(plan.get());
+    if (compile) {
+      std::string log;
+      if (!generic_jit_compile_check(plan.get(), &log)) {
+        text = log;
+        if (buf && cap) {
+          std::strncpy(buf, text.c_str(), cap - 1);
+          buf[cap - 1] = 0;
+        }
+        if (need) *need = text.size() + 1;
+        fail(ErrorKind::Unsupported, "NVRTC could not compile the emitted kernel");
+      }
+    }
+    if (need) *need = text.size() + 1;
+    if (buf && cap) {
+      std::strncpy(buf, text.c_str(), cap - 1);
+      buf[cap - 1] = 0;
+    }
+  });
+}
+
+int pcotgpu_generic_info(const pcotgpu_handle* h, int* mode, int* compiled, char* why, size_t cap) {
+  return guarded([&] {
+    if (!h) fail(ErrorKind::Validation, "null argument");
+    std::string w;
+    h->ex->generic_info(mode, compiled, &w);
+    if (why && cap) {
+      std::strncpy(why, w.c_str(), cap - 1);
+      why[cap - 1] = 0;
+    }
+  });
 }
 
 int pcotgpu_info(const pcotgpu_handle* h, pcotgpu_kernel_info* out) {

@@ -4,6 +4,8 @@
 // point runs the statements that contain it in declaration order, and each
 // body is the postfix program of the reference's flatten (exec.cpp:187-224).
 #include <algorithm>
+#include <cuda.h>
+#include <dlfcn.h>
 #include <climits>
 #include <cstdio>
 #include <cmath>
@@ -11,6 +13,7 @@
 #include <functional>
 #include <map>
 #include <memory>
+#include <mutex>
 #include <numeric>
 
 #include "common.cuh"
@@ -21,129 +24,11 @@ namespace pcotgpu {
 
 namespace {
 
-constexpr int kMaxIdx = 6, kMaxRank = 6, kMaxStack = 32;
-constexpr long long kSpinCapG = 200000000LL;
+#include "generic_dev.cuh"
 
-struct GAff {
-  int64_t c[kMaxIdx];
-  int64_t k;
-};
-// One array reference: storage dims (map composed with the subscripts, params
-// folded) with their modulus / extent / stride, and the logical cell id
-// (row-major over the declared extents, the reference's logical_flat).
-struct GRef {
-  int array, rank, aff0, laff;
-  int64_t ext[kMaxRank], stride[kMaxRank], mod[kMaxRank];
-};
-enum GOpKind { OLit, OAff, ORead, OAdd, OSub, OMul, ODiv, OMin, OMax, ONeg, OSqrt };
-struct GOp {
-  int kind, arg;
-  double lit;
-};
-struct GStmt {
-  int row0, nrows, op0, nops, wref, nreads;
-};
-struct GDev {
-  int nidx, nstmt;
-  int64_t lo[kMaxIdx], ext[kMaxIdx], npoints;
-  const GStmt* st;
-  const GAff* rows;
-  const GAff* affs;
-  const GRef* refs;
-  const GOp* ops;
-  double* const* arr;
-  const int64_t* fbase;  // first flag of each array (logical cells)
-  unsigned* flags;       // dense dataflow: 1 = cell holds its final value; count pass: writes
-  unsigned long long* writer;  // count pass: min over writes of (point * nstmt + statement)
-  unsigned* bad;               // order pass: 1 if a read precedes (or is) its cell's write
-  const int64_t* sbase;  // first shadow of each array (storage cells)
-  long long* shadow;     // mapped dataflow: logical id held by each storage cell
-  const int64_t* lsize;  // logical cells per array
-  int never_ok;          // dense storage: reads of never-written cells see their initial value
-  const int* is_input;   // per array
-  unsigned long long* next;
-  unsigned long long* cnt;  // points, reads, writes
-  int* err;                 // 0 ok; s+1: out-of-extent in statement s; -1: wait cap
-};
-
-PCOT_DEV int64_t aff_eval(const GAff& a, const int64_t* z, int n) {
-  int64_t v = a.k;
-  for (int i = 0; i < n; ++i) v += a.c[i] * z[i];
-  return v;
-}
-
-PCOT_DEV bool in_domain(const GDev& g, const GStmt& s, const int64_t* z) {
-  for (int r = 0; r < s.nrows; ++r)
-    if (aff_eval(g.rows[s.row0 + r], z, g.nidx) < 0) return false;
-  return true;
-}
-
-// Storage cell (reference phys_flat, exec.cpp:310-325): modulo dims wrap,
-// the others must lie inside the map's extents.
-PCOT_DEV bool cell_of(const GDev& g, const GRef& r, const int64_t* z, int64_t* flat) {
-  int64_t f = 0;
-  for (int d = 0; d < r.rank; ++d) {
-    int64_t comp = aff_eval(g.affs[r.aff0 + d], z, g.nidx);
-    if (r.mod[d] > 0) {
-      comp %= r.mod[d];
-      if (comp < 0) comp += r.mod[d];
-    } else if (comp < 0 || comp >= r.ext[d]) {
-      return false;
-    }
-    f += comp * r.stride[d];
-  }
-  *flat = f;
-  return true;
-}
-
-// Logical cell id (reference logical_flat, exec.cpp:327-331); -1 if outside
-// the declared extents (the run then cannot be checked cell by cell).
-PCOT_DEV int64_t logical_of(const GDev& g, const GRef& r, const int64_t* z) {
-  const int64_t l = aff_eval(g.affs[r.laff], z, g.nidx);
-  return l >= 0 && l < g.lsize[r.array] ? l : -1;
-}
-
-PCOT_DEV void decode(const GDev& g, unsigned long long p, int64_t* z) {
-  for (int i = g.nidx - 1; i >= 0; --i) {
-    const unsigned long long e = (unsigned long long)g.ext[i];
-    z[i] = g.lo[i] + int64_t(p % e);
-    p /= e;
-  }
-}
-
-PCOT_DEV unsigned ld_acq_u32(const unsigned* p) {
-  unsigned v;
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-PCOT_DEV void st_rel_u32(unsigned* p, unsigned v) {
-  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-
-PCOT_DEV long long ld_acq_s64(const long long* p) {
-  long long v;
-  asm volatile("ld.acquire.gpu.global.s64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-  return v;
-}
-PCOT_DEV void st_rel_s64(long long* p, long long v) {
-  asm volatile("st.release.gpu.global.s64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-PCOT_DEV void st_rlx_s64(long long* p, long long v) {
-  asm volatile("st.relaxed.gpu.global.s64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-PCOT_DEV double ld_acq_f64(const double* p) {
-  double v;
-  asm volatile("ld.acquire.gpu.global.f64 %0, [%1];" : "=d"(v) : "l"(p) : "memory");
-  return v;
-}
-PCOT_DEV void st_rel_f64(double* p, double v) {
-  asm volatile("st.release.gpu.global.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
-}
-
-// Run every statement of point z.  Returns false on an error (recorded).
-// DATAFLOW: 0 sequential; 1 dense storage, per-cell ready flags; 2 mapped
-// storage, per-storage-cell shadows holding the logical id of the value they
-// hold (the reference's shadow array, exec.cpp:360-368, used as the wait).
+// Run every statement of point z (interpreter: the reference's postfix
+// program, exec.cpp:187-224, one rounding per operation).  Returns false on an
+// error (recorded).
 template <int DATAFLOW>
 PCOT_DEV bool exec_point(const GDev& g, const int64_t* z, unsigned long long* c3) {
   for (int si = 0; si < g.nstmt; ++si) {
@@ -157,59 +42,10 @@ PCOT_DEV bool exec_point(const GDev& g, const int64_t* z, unsigned long long* c3
         case OLit: stk[sp++] = op.lit; break;
         case OAff: stk[sp++] = double(aff_eval(g.affs[op.arg], z, g.nidx)); break;
         case ORead: {
-          const GRef& r = g.refs[op.arg];
-          int64_t f = 0;
-          if (!cell_of(g, r, z, &f)) {
-            atomicCAS(g.err, 0, si + 1);
-            return false;
-          }
-          if (DATAFLOW == 1) {
-            const unsigned* fl = g.flags + g.fbase[r.array] + f;
-            long long it = 0;
-            while (ld_acq_u32(fl) == 0) {
-              if (++it > kSpinCapG) {
-                atomicCAS(g.err, 0, -1);
-                return false;
-              }
-              // a failed point never publishes its cell: stop waiting on error
-              if ((it & 255) == 0 && *reinterpret_cast<volatile int*>(g.err) != 0) return false;
-              __nanosleep(64);
-            }
-          }
-          if (DATAFLOW == 2) {
-            // wait until the storage cell holds this logical cell's value ...
-            const long long want = logical_of(g, r, z);
-            const long long* sh = g.shadow + g.sbase[r.array] + f;
-            const unsigned long long* wk = g.writer + g.fbase[r.array];
-            long long it = 0;
-            for (long long held; (held = ld_acq_s64(sh)) != want;) {
-              // the cell holds a LATER occupant (its write comes after ours in
-              // the reference's order): our value was overwritten before this
-              // read — the fold is not universal for this kernel
-              if (held >= 0 && wk[held] > wk[want]) {
-                atomicCAS(g.err, 0, -2);
-                return false;
-              }
-              if (++it > kSpinCapG) {
-                atomicCAS(g.err, 0, -1);
-                return false;
-              }
-              if ((it & 255) == 0 && *reinterpret_cast<volatile int*>(g.err) != 0) return false;
-              __nanosleep(64);
-            }
-            // (seqlock: a writer invalidates the shadow before its data store,
-            // so a load that saw new data also sees the changed shadow)
-            const double v = ld_acq_f64(g.arr[r.array] + f);
-            // ... and still does after the load: a map that is not a universal
-            // occupancy vector could let a later write reuse the cell early
-            if (ld_acq_s64(sh) != want) {
-              atomicCAS(g.err, 0, -2);
-              return false;
-            }
-            stk[sp++] = v;
-            break;
-          }
-          stk[sp++] = __ldcg(g.arr[r.array] + f);
+          bool ok = true;
+          const double v = gread<DATAFLOW>(g, op.arg, z, si, ok);
+          if (!ok) return false;
+          stk[sp++] = v;
           break;
         }
         case OAdd: --sp, stk[sp - 1] = __dadd_rn(stk[sp - 1], stk[sp]); break;
@@ -230,27 +66,20 @@ PCOT_DEV bool exec_point(const GDev& g, const int64_t* z, unsigned long long* c3
         case OSqrt: stk[sp - 1] = __dsqrt_rn(stk[sp - 1]); break;
       }
     }
-    const GRef& w = g.refs[s.wref];
-    int64_t f = 0;
-    if (!cell_of(g, w, z, &f)) {
-      atomicCAS(g.err, 0, si + 1);
-      return false;
-    }
-    if (DATAFLOW == 2) {  // invalidate, data, publish (see the reader's seqlock)
-      long long* sh = g.shadow + g.sbase[w.array] + f;
-      st_rlx_s64(sh, -2);
-      st_rel_f64(g.arr[w.array] + f, stk[sp - 1]);
-      st_rel_s64(sh, logical_of(g, w, z));
-    } else {
-      __stcg(g.arr[w.array] + f, stk[sp - 1]);
-    }
-    if (DATAFLOW == 1) st_rel_u32(g.flags + g.fbase[w.array] + f, 1u);
+    if (!gwrite<DATAFLOW>(g, s.wref, z, si, stk[sp - 1])) return false;
     c3[0] += 1;
     c3[1] += unsigned(s.nreads);
     c3[2] += 1;
   }
   return true;
 }
+
+struct InterpPE {
+  template <int MODE>
+  static PCOT_DEV bool run(const GDev& g, const int64_t* z, unsigned long long* c3) {
+    return exec_point<MODE>(g, z, c3);
+  }
+};
 
 __global__ void generic_count_kernel(GDev g) {
   int64_t z[kMaxIdx];
@@ -333,48 +162,12 @@ __global__ void generic_shadow_init_kernel(long long* sh, int64_t n, int64_t bas
     sh[base + i] = is_input ? i : -1;
 }
 
-// Persistent dataflow grid: warps take 32 consecutive points in the
-// reference's order; reads wait for their cell's flag (dense) or shadow (mapped).
 template <int MODE>
 __global__ void generic_dataflow_kernel(GDev g) {
-  const int lane = threadIdx.x & 31;
-  unsigned long long c3[3] = {0, 0, 0};
-  int64_t z[kMaxIdx];
-  bool ok = true;
-  for (;;) {
-    unsigned long long base = 0;
-    if (lane == 0) base = atomicAdd(g.next, 32ull);
-    base = __shfl_sync(0xffffffffu, base, 0);
-    if (base >= (unsigned long long)g.npoints) break;
-    const unsigned long long p = base + lane;
-    if (ok && p < (unsigned long long)g.npoints) {
-      decode(g, p, z);
-      ok = exec_point<MODE>(g, z, c3);
-    }
-  }
-  atomicAdd(&g.cnt[0], c3[0]);
-  atomicAdd(&g.cnt[1], c3[1]);
-  atomicAdd(&g.cnt[2], c3[2]);
+  dataflow_loop<MODE, InterpPE>(g);
 }
 
-// One thread, the reference's exact order (kernels that overwrite cells).
-__global__ void generic_sequential_kernel(GDev g) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
-  unsigned long long c3[3] = {0, 0, 0};
-  int64_t z[kMaxIdx];
-  if (g.npoints > 0) decode(g, 0, z);
-  for (unsigned long long p = 0; p < (unsigned long long)g.npoints; ++p) {
-    if (!exec_point<0>(g, z, c3)) break;
-    // next point in lexicographic order (odometer: no 64-bit divisions)
-    for (int i = g.nidx - 1; i >= 0; --i) {
-      if (++z[i] < g.lo[i] + g.ext[i]) break;
-      z[i] = g.lo[i];
-    }
-  }
-  g.cnt[0] = c3[0];
-  g.cnt[1] = c3[1];
-  g.cnt[2] = c3[2];
-}
+__global__ void generic_sequential_kernel(GDev g) { sequential_loop<InterpPE>(g); }
 
 // ---------------------------------------------------------------- host side
 int64_t floor_div(int64_t a, int64_t b) {  // b > 0
@@ -467,6 +260,12 @@ struct GenericPlan {
   unsigned long long* d_writer = nullptr;
   bool dataflow = false;
   bool counted = false;
+  // PRDG -> CUDA emitter: the plan's statements as straight-line device code,
+  // compiled at run time (NVRTC); null when unavailable (interpreter then)
+  std::string jit_src, jit_why;
+  void* jit_module = nullptr;  // CUmodule
+  void* jit_fn[3] = {nullptr, nullptr, nullptr};  // sequential, dataflow flags, dataflow shadows
+  bool jit_tried = false;
 };
 
 namespace {
@@ -511,14 +310,14 @@ int64_t eval_extent(const Affine& a, size_t nidx, const IntVec& prm) {
 }  // namespace
 
 GenericPlan* generic_plan_create(const KernelSpec& k, const IntVec& prm,
-                                 const std::vector<MemoryMap>& maps, int device) {
+                                 const std::vector<MemoryMap>& maps, int device, bool host_only) {
   if (prm.size() != k.params.size()) fail(ErrorKind::DimMismatch, "GpuExecutor: parameter count");
   const size_t full = k.indices.size();
   if (full == 0 || full > size_t(kMaxIdx)) fail(ErrorKind::Unsupported, "generic executor: 1..6 indices");
   auto P = std::make_unique<GenericPlan>();
   P->device = device;
   P->nidx = int(full);
-  ckc(cudaSetDevice(device), "cudaSetDevice");
+  if (!host_only) ckc(cudaSetDevice(device), "cudaSetDevice");
   // ---- arrays: storage by the caller's memory map (reference exec.cpp:
   // 234-245, MemoryMap::words), else dense at the declared extents
   auto map_of = [&](const std::string& name) -> const MemoryMap* {
@@ -561,7 +360,7 @@ GenericPlan* generic_plan_create(const KernelSpec& k, const IntVec& prm,
     fb += int64_t(lw);
     sb += int64_t(w);
     double* d = nullptr;
-    ckc(cudaMalloc(&d, std::max<uint64_t>(w, 1) * 8), "cudaMalloc");
+    if (!host_only) ckc(cudaMalloc(&d, std::max<uint64_t>(w, 1) * 8), "cudaMalloc");
     P->ptrs.push_back(d);
   }
   P->nflags = fb;
@@ -716,6 +515,7 @@ GenericPlan* generic_plan_create(const KernelSpec& k, const IntVec& prm,
       P->npoints *= P->ext[q];
     }
   }
+  if (host_only) return P.release();  // tables only (the emitter's source)
   P->d_st = upload(P->st);
   P->d_rows = upload(P->rows);
   P->d_affs = upload(P->affs);
@@ -740,8 +540,280 @@ GenericPlan* generic_plan_create(const KernelSpec& k, const IntVec& prm,
   return P.release();
 }
 
+// ---------------------------------------------------------------- PRDG -> CUDA emitter
+// The GPU analogue of the reference's emit_c (emit_c.cpp:191-262): every
+// statement of the plan becomes straight-line device code — its domain rows
+// as constant affine tests, its body as one IEEE-rounded intrinsic per
+// operation in the reference's postfix order (exec.cpp:187-224), its reads
+// and write through the shared runtime (generic_dev.cuh: map addressing and
+// the schedule's wait / publish protocol).  Compiled at run time with NVRTC
+// for sm_100a and launched in place of the interpreter kernels; no operand
+// stack, no per-operation dispatch.
+
+static const char kGenericDevSrc[] =
+#include "generic_dev_src.inc"
+    ;
+
+namespace {
+
+std::string aff_src(const GAff& a, int nidx) {
+  std::string e;
+  for (int i = 0; i < nidx; ++i)
+    if (a.c[i]) e += " + (" + std::to_string((long long)a.c[i]) + "LL * z[" + std::to_string(i) + "])";
+  e += " + (" + std::to_string((long long)a.k) + "LL)";
+  return "(0LL" + e + ")";
+}
+
+std::string lit_src(double v) {
+  char b[64];
+  std::snprintf(b, sizeof b, "%a", v);
+  return std::string("(") + b + ")";
+}
+
+struct NvrtcApi {
+  void* h = nullptr;
+  int (*create)(void**, const char*, const char*, int, const char* const*, const char* const*) = nullptr;
+  int (*compile)(void*, int, const char* const*) = nullptr;
+  int (*log_size)(void*, size_t*) = nullptr;
+  int (*log)(void*, char*) = nullptr;
+  int (*cubin_size)(void*, size_t*) = nullptr;
+  int (*cubin)(void*, char*) = nullptr;
+  int (*destroy)(void**) = nullptr;
+  bool ok = false;
+};
+
+const NvrtcApi& nvrtc() {
+  static const NvrtcApi api = [] {
+    NvrtcApi a;
+    a.h = dlopen("libnvrtc.so.12", RTLD_NOW | RTLD_LOCAL);
+    if (!a.h) a.h = dlopen("libnvrtc.so", RTLD_NOW | RTLD_LOCAL);
+    if (!a.h) return a;
+    a.create = reinterpret_cast<decltype(a.create)>(dlsym(a.h, "nvrtcCreateProgram"));
+    a.compile = reinterpret_cast<decltype(a.compile)>(dlsym(a.h, "nvrtcCompileProgram"));
+    a.log_size = reinterpret_cast<decltype(a.log_size)>(dlsym(a.h, "nvrtcGetProgramLogSize"));
+    a.log = reinterpret_cast<decltype(a.log)>(dlsym(a.h, "nvrtcGetProgramLog"));
+    a.cubin_size = reinterpret_cast<decltype(a.cubin_size)>(dlsym(a.h, "nvrtcGetCUBINSize"));
+    a.cubin = reinterpret_cast<decltype(a.cubin)>(dlsym(a.h, "nvrtcGetCUBIN"));
+    a.destroy = reinterpret_cast<decltype(a.destroy)>(dlsym(a.h, "nvrtcDestroyProgram"));
+    a.ok = a.create && a.compile && a.log_size && a.log && a.cubin_size && a.cubin && a.destroy;
+    return a;
+  }();
+  return api;
+}
+
+struct DriverApi {
+  CUresult (*load)(CUmodule*, const void*) = nullptr;
+  CUresult (*get)(CUfunction*, CUmodule, const char*) = nullptr;
+  CUresult (*launch)(CUfunction, unsigned, unsigned, unsigned, unsigned, unsigned, unsigned, unsigned,
+                     CUstream, void**, void**) = nullptr;
+  CUresult (*unload)(CUmodule) = nullptr;
+  bool ok = false;
+};
+
+const DriverApi& driver() {
+  static const DriverApi api = [] {
+    DriverApi a;
+    auto sym = [](const char* n) -> void* {
+      void* fn = nullptr;
+      cudaDriverEntryPointQueryResult q;
+      if (cudaGetDriverEntryPoint(n, &fn, cudaEnableDefault, &q) != cudaSuccess ||
+          q != cudaDriverEntryPointSuccess)
+        return nullptr;
+      return fn;
+    };
+    a.load = reinterpret_cast<decltype(a.load)>(sym("cuModuleLoadData"));
+    a.get = reinterpret_cast<decltype(a.get)>(sym("cuModuleGetFunction"));
+    a.launch = reinterpret_cast<decltype(a.launch)>(sym("cuLaunchKernel"));
+    a.unload = reinterpret_cast<decltype(a.unload)>(sym("cuModuleUnload"));
+    a.ok = a.load && a.get && a.launch && a.unload;
+    return a;
+  }();
+  return api;
+}
+
+// compiled modules by (device, source): kept for the process (a module is a
+// few tens of KB; plans of the same kernel and binding reuse it)
+std::mutex& jit_cache_mu() {
+  static std::mutex m;
+  return m;
+}
+std::map<std::pair<int, std::string>, CUmodule>& jit_cache() {
+  static std::map<std::pair<int, std::string>, CUmodule> c;
+  return c;
+}
+
+}  // namespace
+
+// Source of the plan's kernels (host only: no device needed).
+std::string generic_emit_source(const GenericPlan* P) {
+  std::string o;
+  o += "#define PCOT_DEV __device__ __forceinline__\n";
+  o += "typedef long long int64_t;\n";
+  o += kGenericDevSrc;
+  o += "\nstruct JitPE {\n  template <int MODE>\n"
+       "  static PCOT_DEV bool run(const GDev& g, const int64_t* z, unsigned long long* c3) {\n";
+  for (size_t si = 0; si < P->st.size(); ++si) {
+    const GStmt& st = P->st[si];
+    o += "    // statement " + P->stmt_ids[si] + "\n    if (1";
+    for (int r = 0; r < st.nrows; ++r) o += "\n        && " + aff_src(P->rows[size_t(st.row0 + r)], P->nidx) + " >= 0LL";
+    o += ") {\n      bool ok = true;\n";
+    std::vector<std::string> stk;
+    int t = 0;
+    for (int q = st.op0; q < st.op0 + st.nops; ++q) {
+      const GOp& op = P->ops[size_t(q)];
+      const std::string v = "t" + std::to_string(t++);
+      std::string e;
+      auto pop = [&]() { std::string x = stk.back(); stk.pop_back(); return x; };
+      switch (op.kind) {
+        case OLit: e = lit_src(op.lit); break;
+        case OAff: e = "(double)" + aff_src(P->affs[size_t(op.arg)], P->nidx); break;
+        case ORead:
+          o += "      const double " + v + " = gread<MODE>(g, " + std::to_string(op.arg) + ", z, " +
+               std::to_string(si) + ", ok);\n      if (!ok) return false;\n";
+          stk.push_back(v);
+          continue;
+        case OAdd: { const std::string b = pop(), a = pop(); e = "__dadd_rn(" + a + ", " + b + ")"; break; }
+        case OSub: { const std::string b = pop(), a = pop(); e = "__dsub_rn(" + a + ", " + b + ")"; break; }
+        case OMul: { const std::string b = pop(), a = pop(); e = "__dmul_rn(" + a + ", " + b + ")"; break; }
+        case ODiv: { const std::string b = pop(), a = pop(); e = "__ddiv_rn(" + a + ", " + b + ")"; break; }
+        case OMin: { const std::string b = pop(), a = pop(); e = "(" + b + " < " + a + " ? " + b + " : " + a + ")"; break; }
+        case OMax: { const std::string b = pop(), a = pop(); e = "(" + a + " < " + b + " ? " + b + " : " + a + ")"; break; }
+        case ONeg: e = "(-" + pop() + ")"; break;
+        case OSqrt: e = "__dsqrt_rn(" + pop() + ")"; break;
+      }
+      o += "      const double " + v + " = " + e + ";\n";
+      stk.push_back(v);
+    }
+    o += "      if (!gwrite<MODE>(g, " + std::to_string(st.wref) + ", z, " + std::to_string(si) + ", " +
+         stk.back() + ")) return false;\n";
+    o += "      c3[0] += 1; c3[1] += " + std::to_string(st.nreads) + "; c3[2] += 1;\n    }\n";
+  }
+  o += "    return true;\n  }\n};\n";
+  o += "extern \"C\" __global__ void pcot_jit_seq(GDev g) { sequential_loop<JitPE>(g); }\n";
+  o += "extern \"C\" __global__ void pcot_jit_df1(GDev g) { dataflow_loop<1, JitPE>(g); }\n";
+  o += "extern \"C\" __global__ void pcot_jit_df2(GDev g) { dataflow_loop<2, JitPE>(g); }\n";
+  return o;
+}
+
+// Compile + load the plan's kernels once; false (with the reason) when NVRTC
+// or the driver entry points are unavailable or compilation fails.
+bool generic_jit_build(GenericPlan* P) {
+  if (P->jit_tried) return P->jit_module != nullptr;
+  P->jit_tried = true;
+  if (env_int("PCOTGPU_GENERIC_JIT", 1) == 0) {
+    P->jit_why = "disabled (PCOTGPU_GENERIC_JIT=0)";
+    return false;
+  }
+  const NvrtcApi& nv = nvrtc();
+  const DriverApi& dr = driver();
+  if (!nv.ok || !dr.ok) {
+    P->jit_why = !nv.ok ? "libnvrtc not loadable" : "driver entry points unavailable";
+    return false;
+  }
+  P->jit_src = generic_emit_source(P);
+  CUmodule cached = nullptr;
+  {  // one compile per (device, source) and process: plans of the same kernel share it
+    std::lock_guard<std::mutex> lk(jit_cache_mu());
+    auto it = jit_cache().find({P->device, P->jit_src});
+    if (it != jit_cache().end()) cached = it->second;
+  }
+  if (cached) {
+    const char* names[3] = {"pcot_jit_seq", "pcot_jit_df1", "pcot_jit_df2"};
+    for (int q = 0; q < 3; ++q) {
+      CUfunction f = nullptr;
+      if (dr.get(&f, cached, names[q]) != CUDA_SUCCESS) {
+        P->jit_why = std::string("cuModuleGetFunction ") + names[q];
+        return false;
+      }
+      P->jit_fn[q] = f;
+    }
+    P->jit_module = cached;
+    P->jit_why = "compiled (cached)";
+    return true;
+  }
+  void* prog = nullptr;
+  if (nv.create(&prog, P->jit_src.c_str(), "pcot_generic.cu", 0, nullptr, nullptr) != 0) {
+    P->jit_why = "nvrtcCreateProgram failed";
+    return false;
+  }
+  const char* opts[] = {"--gpu-architecture=sm_100a", "-std=c++17", "--fmad=false", "-lineinfo"};
+  const int rc = nv.compile(prog, 4, opts);
+  if (rc != 0) {
+    size_t n = 0;
+    nv.log_size(prog, &n);
+    std::string lg(n, '\0');
+    nv.log(prog, &lg[0]);
+    P->jit_why = "NVRTC: " + lg.substr(0, 2000);
+    nv.destroy(&prog);
+    return false;
+  }
+  size_t n = 0;
+  nv.cubin_size(prog, &n);
+  std::vector<char> cubin(n);
+  nv.cubin(prog, cubin.data());
+  nv.destroy(&prog);
+  cudaSetDevice(P->device);
+  cudaFree(nullptr);  // the runtime's primary context is current
+  CUmodule m = nullptr;
+  if (dr.load(&m, cubin.data()) != CUDA_SUCCESS) {
+    P->jit_why = "cuModuleLoadData failed";
+    return false;
+  }
+  {
+    std::lock_guard<std::mutex> lk(jit_cache_mu());
+    jit_cache()[{P->device, P->jit_src}] = m;
+  }
+  const char* names[3] = {"pcot_jit_seq", "pcot_jit_df1", "pcot_jit_df2"};
+  for (int q = 0; q < 3; ++q) {
+    CUfunction f = nullptr;
+    if (dr.get(&f, m, names[q]) != CUDA_SUCCESS) {
+      dr.unload(m);
+      P->jit_why = std::string("cuModuleGetFunction ") + names[q];
+      return false;
+    }
+    P->jit_fn[q] = f;
+  }
+  P->jit_module = m;
+  P->jit_why = "compiled";
+  return true;
+}
+
+const std::string& generic_jit_status(const GenericPlan* p) { return p->jit_why; }
+
+// Host only: emit and NVRTC-compile the plan's kernels (no module load).
+bool generic_jit_compile_check(const GenericPlan* P, std::string* log) {
+  const NvrtcApi& nv = nvrtc();
+  if (!nv.ok) {
+    if (log) *log = "libnvrtc not loadable";
+    return false;
+  }
+  const std::string src = generic_emit_source(P);
+  void* prog = nullptr;
+  if (nv.create(&prog, src.c_str(), "pcot_generic.cu", 0, nullptr, nullptr) != 0) return false;
+  const char* opts[] = {"--gpu-architecture=sm_100a", "-std=c++17", "--fmad=false"};
+  const int rc = nv.compile(prog, 3, opts);
+  size_t n = 0;
+  nv.log_size(prog, &n);
+  std::string lg(n, '\0');
+  if (n) nv.log(prog, &lg[0]);
+  size_t cb = 0;
+  if (rc == 0) nv.cubin_size(prog, &cb);
+  nv.destroy(&prog);
+  if (log) *log = lg;
+  return rc == 0 && cb > 0;
+}
+
+static cudaError_t jit_launch(GenericPlan* P, int q, unsigned grid, unsigned block, GDev g, cudaStream_t s) {
+  void* args[] = {&g};
+  const CUresult r = driver().launch(static_cast<CUfunction>(P->jit_fn[q]), grid, 1, 1, block, 1, 1, 0,
+                                     reinterpret_cast<CUstream>(s), args, nullptr);
+  count_launch();
+  return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorLaunchFailure;
+}
+
 void generic_plan_destroy(GenericPlan* p) {
   if (!p) return;
+  // (compiled modules stay in the process-wide cache)
   for (double* d : p->ptrs) cudaFree(d);
   cudaFree(p->d_st);
   cudaFree(p->d_rows);
@@ -880,10 +952,15 @@ cudaError_t generic_run(GenericPlan* p, cudaStream_t s, GenericCounts* counts, s
       count_launch();
     }
   }
+  const bool jit = p->npoints > 0 && generic_jit_build(p);
   if (p->npoints > 0) {
     if (p->dataflow && p->mapped) {
-      generic_dataflow_kernel<2><<<sms * 4, 128, 0, s>>>(g);
-      count_launch();
+      if (jit) {
+        if ((e = jit_launch(p, 2, unsigned(sms * 4), 128, g, s)) != cudaSuccess) return e;
+      } else {
+        generic_dataflow_kernel<2><<<sms * 4, 128, 0, s>>>(g);
+        count_launch();
+      }
       // a storage cell reused under a waiting reader (the map folds along a
       // vector that is not universal for this kernel's dependences): this run
       // is void; the plan switches to the reference's sequential order for
@@ -898,11 +975,20 @@ cudaError_t generic_run(GenericPlan* p, cudaStream_t s, GenericCounts* counts, s
         return generic_run(p, s, counts, err_msg);
       }
     } else if (p->dataflow) {
-      generic_dataflow_kernel<1><<<sms * 4, 128, 0, s>>>(g);
+      if (jit) {
+        if ((e = jit_launch(p, 1, unsigned(sms * 4), 128, g, s)) != cudaSuccess) return e;
+      } else {
+        generic_dataflow_kernel<1><<<sms * 4, 128, 0, s>>>(g);
+        count_launch();
+      }
     } else {
-      generic_sequential_kernel<<<1, 32, 0, s>>>(g);
+      if (jit) {
+        if ((e = jit_launch(p, 0, 1, 32, g, s)) != cudaSuccess) return e;
+      } else {
+        generic_sequential_kernel<<<1, 32, 0, s>>>(g);
+        count_launch();
+      }
     }
-    if (!(p->dataflow && p->mapped)) count_launch();
   }
   unsigned long long c[3] = {0, 0, 0};
   int err = 0;
@@ -923,6 +1009,7 @@ cudaError_t generic_run(GenericPlan* p, cudaStream_t s, GenericCounts* counts, s
     counts->writes = c[2];
     counts->parallel = p->dataflow;
     counts->mode = !p->dataflow ? 0 : p->mapped ? 2 : 1;
+    counts->compiled = p->jit_module != nullptr;
   }
   return cudaSuccess;
 }

@@ -46,8 +46,10 @@ struct GenericPlan;
 // `maps` (may be empty): the reference's MemoryMaps — storage of each mapped
 // array is laid out exactly by its map (words, modulo folding, extents), as the
 // reference's ArrayStore is; unmapped arrays are dense at declared extents.
+// host_only: the plan tables without device storage (the emitter's source).
 GenericPlan* generic_plan_create(const KernelSpec& k, const IntVec& params,
-                                 const std::vector<MemoryMap>& maps, int device);
+                                 const std::vector<MemoryMap>& maps, int device,
+                                 bool host_only = false);
 void generic_plan_destroy(GenericPlan* p);
 
 // Array access (dense, declaration extents).
@@ -64,9 +66,19 @@ struct GenericCounts {
   uint64_t points = 0, reads = 0, writes = 0;
   bool parallel = false;  // dataflow grid (true) or sequential walk
   int mode = 0;           // 0 sequential, 1 dataflow over dense flags, 2 dataflow over shadows
+  bool compiled = false;  // the emitter's NVRTC-compiled kernels ran (else the interpreter)
 };
 // One run.  Errors: cudaErrorInvalidValue with `err_msg` set for an
 // out-of-extent access (reference exec.cpp:318-323).
 cudaError_t generic_run(GenericPlan* p, cudaStream_t s, GenericCounts* counts, std::string* err_msg);
+
+// PRDG -> CUDA emitter (the GPU analogue of the reference's emit_c): the
+// plan's statements as device source (host only), and its NVRTC build; the
+// runs use the compiled kernels when the build succeeds (PCOTGPU_GENERIC_JIT=0:
+// interpreter).  generic_jit_status: "compiled" or why not.
+std::string generic_emit_source(const GenericPlan* p);
+bool generic_jit_build(GenericPlan* p);
+const std::string& generic_jit_status(const GenericPlan* p);
+bool generic_jit_compile_check(const GenericPlan* p, std::string* log);
 
 }  // namespace pcotgpu
