@@ -18,6 +18,10 @@
 
 namespace pcotgpu {
 
+// dgemm_tma.cu: tensor-TMA + mbarrier-ring kernel (the default).
+cudaError_t dgemm_nn_tma(const double* A, const double* B, double* C, int64_t n, int64_t ld,
+                         int order, int variant, cudaStream_t stream);
+
 namespace {
 
 constexpr int BM = 128, BN = 128;
@@ -186,6 +190,10 @@ cudaError_t dgemm_nn(const double* A, const double* B, double* C, int64_t n, int
   const int tiles_m = int((n + BM - 1) / BM), tiles_n = int((n + BN - 1) / BN);
   const int grid = tiles_m * tiles_n;  // both orders (compact Morton rank for COT)
   const int variant = env_int("PCOTGPU_DGEMM_VARIANT", 0);  // 0: default
+  // 0 / 10: the TMA kernel (BK 32 x 3 stages / BK 16 x 6 stages); 1-9: the
+  // cp.async kernels of round 1 (9 = their best, the previous default)
+  if (variant == 0 || variant == 10)
+    return dgemm_nn_tma(A, B, C, n, ld, order, variant == 10 ? 1 : 0, stream);
   // measured on the B200 at N=4096 (tools/kbench.py gemm; profiles/dgemm_r01.md)
   switch (variant) {
     case 1: return launch_gemm<GemmCfg<2, 4, 16, 4>>(A, B, C, n, ld, order, tiles_m, tiles_n, grid, stream);  // 28.2 TF/s
