@@ -377,6 +377,16 @@ def per_config(P, torch, dev, local, hbm_peak, reps_ms=1000.0):
                                      "latency_bound_ms_at_max_clock": round(steps * fl * lat / 1965e3, 4),
                                      "latency_frac": round(steps * fl * lat / 1965e3 / ms, 3),
                                      "launches_per_run": int(first.launches)}
+                elif first.bt == 0:
+                    # on-chip resident run (stencil2d_res.cu): the grid crosses HBM
+                    # once per run (16/T B/update), so the bound is on-chip: the
+                    # 5 fp64 operations per update against the measured DADD issue
+                    dadd_peak = 18.4e12  # profiles/fp64_peaks_r01.json
+                    e["roofline"] = {"bound": "fp64 issue (grid resident in shared memory, one launch)",
+                                     "fp64_ops_per_update": 5.0, "achieved": round(gu * 5.0, 1),
+                                     "peak": dadd_peak / 1e9, "unit": "Gop/s",
+                                     "frac": round(gu * 5.0e9 / dadd_peak, 3),
+                                     "hbm_bytes_per_update": round(16.0 / params["T"], 4)}
                 else:
                     bpu = 16.0 / first.bt
                     e["roofline"] = {"bound": "hbm", "bytes_per_update": bpu, "achieved": round(gu * bpu, 1),

@@ -18,10 +18,6 @@
 
 namespace pcotgpu {
 
-// dgemm_tma.cu: tensor-TMA + mbarrier-ring kernel (the default).
-cudaError_t dgemm_nn_tma(const double* A, const double* B, double* C, int64_t n, int64_t ld,
-                         int order, int variant, cudaStream_t stream);
-
 namespace {
 
 constexpr int BM = 128, BN = 128;

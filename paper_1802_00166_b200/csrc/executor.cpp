@@ -79,6 +79,8 @@ struct GpuExecutor::Impl {
   DevBuf gsa;
   int64_t gs_ld = 0;
   GsPlan* gs_plan = nullptr;
+  S2ResPlan* res_plan = nullptr;  // on-chip resident 2-D stencil (small grids)
+  bool res_tried = false;
   int gs_cfg[3] = {0, 0, 0};
   int gs_pipe_ok = -1;
   // GEMM
@@ -106,6 +108,7 @@ struct GpuExecutor::Impl {
     if (h2d) cudaStreamDestroy(h2d);
     if (d2h) cudaStreamDestroy(d2h);
     if (gs_plan) gs2d_plan_destroy(gs_plan);
+    if (res_plan) s2d5_res_destroy(res_plan);
     if (gplan) generic_plan_destroy(gplan);
     if (ev0) cudaEventDestroy(ev0);
     if (ev1) cudaEventDestroy(ev1);
@@ -247,6 +250,23 @@ struct GpuExecutor::Impl {
     const int order = o.scheme == Scheme::Cot ? kOrderMorton : kOrderLex;
     ck(copy_rows(sg[0].origin, sg[0].ld, in[0].p, in_ld, n, n, stream), "copy_rows");
     if (!rec.ring_hold) ck(zero_ring_2d(sg[0].origin, sg[0].ld, n, stream), "zero_ring");
+    // Opt-in experiment (PCOTGPU_RESIDENT=1, untiled schedule, grids up to 2048^2):
+    // one persistent launch keeps every row band in shared memory for all T
+    // steps (stencil2d_res.cu).  Bit-exact, but measured slower than the
+    // streaming kernel on the B200 (2048^2 T=256: 2.2 ms vs 1.19 ms): the
+    // band-to-band row exchange moves 19 MB through L2 per step
+    // (profiles/cfg0_resident_r02.md), so the default stays the streaming path.
+    if (o.scheme == Scheme::Untiled && T >= 4 && env_int("PCOTGPU_RESIDENT", 0) != 0) {
+      if (!res_tried) {
+        res_tried = true;
+        res_plan = s2d5_res_create(n, device);
+      }
+      if (res_plan) {
+        ck(s2d5_res_run(res_plan, sg[0], sg[1], T, stream), "s2d5_res_run");
+        result_slot = 1;
+        return 0;  // no depth blocks: the whole run is one launch
+      }
+    }
     if (o.scheme == Scheme::Cot && o.space_time && T > 0) {
       // Space-time recursive order (reference cot_order over the band box with
       // time, tiler.cpp:150-203, 98-117): cells (d, r) = (depth block, row band).
@@ -315,6 +335,9 @@ struct GpuExecutor::Impl {
   void check_gs_fault() {
     if (rec.family == Family::GaussSeidel2D9 && gs_plan && gs2d_plan_fault(gs_plan))
       ck(cudaErrorLaunchTimeout, "Gauss-Seidel: a dependence wait hit its spin cap "
+                                 "(CTAs not co-resident?); the grid is invalid");
+    if (rec.family == Family::Stencil2D5 && res_plan && s2d5_res_fault(res_plan))
+      ck(cudaErrorLaunchTimeout, "resident stencil: a neighbour-band wait hit its spin cap "
                                  "(CTAs not co-resident?); the grid is invalid");
   }
 

@@ -35,6 +35,20 @@ cudaError_t s2d5_advance_p2p(const Slab2D& in, const Slab2D& out, int64_t g0, in
                              double* mirror_up, double* mirror_dn, int mirror_rows,
                              cudaStream_t stream);
 int s2d5_max_bt();
+// Grid resident on chip for the whole run (stencil2d_res.cu): one persistent
+// CTA per SM owns a band of rows in shared memory and steps it T times;
+// neighbours exchange boundary rows through flags (no grid barrier).  create()
+// returns null when the grid does not fit (n outside [64, 2048], band larger
+// than shared memory, no cooperative launch).  `in` must hold the step-0 grid
+// with its ring already zeroed / held; `out` receives step T.
+struct S2ResPlan;
+S2ResPlan* s2d5_res_create(int64_t n, int device);
+void s2d5_res_destroy(S2ResPlan* p);
+cudaError_t s2d5_res_run(S2ResPlan* p, const Slab2D& in, const Slab2D& out, int64_t T,
+                         cudaStream_t stream);
+// Nonzero if a neighbour wait of the runs since the last call hit its spin cap
+// (the grid is then invalid); call after synchronising the run's stream.
+int s2d5_res_fault(S2ResPlan* p);
 // Programmatic dependent launch for the stencil depth blocks (PCOTGPU_PDL=0: off).
 bool pdl_enabled();
 
@@ -70,6 +84,10 @@ cudaError_t div9_check(const double* x, double* q_fast, double* q_ref, int64_t n
 // C = A*B, fp64 DMMA tensor cores, row-major N x N with pitch ld.
 cudaError_t dgemm_nn(const double* A, const double* B, double* C, int64_t n, int64_t ld,
                      int order, cudaStream_t stream);
+// The tensor-TMA + mbarrier-ring kernel behind dgemm_nn's default (dgemm_tma.cu);
+// variant 0: BK 32 x 3 stages, 1: BK 16 x 6 stages.
+cudaError_t dgemm_nn_tma(const double* A, const double* B, double* C, int64_t n, int64_t ld,
+                         int order, int variant, cudaStream_t stream);
 // y = 2x - 1 elementwise (exact for x in [0,1) of the reference init_value).
 cudaError_t affine_2x_minus_1(const double* x, double* y, int64_t count, cudaStream_t stream);
 

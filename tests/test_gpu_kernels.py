@@ -258,3 +258,37 @@ def test_executors_on_concurrent_host_threads():
     assert not errors, errors
     for key, w in want.items():
         assert got[key] == {w}, key
+
+
+# ---------------------------------------------------------------- resident 2-D stencil
+@pytest.mark.parametrize("kernel", ["jacobi2d", "heat2d_hold"])
+@pytest.mark.parametrize("N,T", [(64, 4), (100, 7), (127, 9), (130, 16), (296, 5), (500, 33),
+                                 (1000, 40), (1024, 12), (2047, 6), (2048, 10)])
+def test_resident_stencil_matches_oracle(monkeypatch, kernel, N, T):
+    """The on-chip resident kernel (PCOTGPU_RESIDENT=1, untiled schedule of
+    grids up to 2048^2, stencil2d_res.cu) against the oracle, bit for bit:
+    ragged widths, bands of 2..14 rows, odd and even step counts; and the
+    streaming kernel on the same executor gives the same bits."""
+    monkeypatch.setenv("PCOTGPU_RESIDENT", "1")
+    want = O.reference_output(kernel, {"T": T, "N": N})
+    with P.GpuExecutor(kernel, {"T": T, "N": N}) as ex:
+        r = ex.run_untiled()
+        assert r.bt == 0 and r.launches <= 4  # one persistent launch (+ copy-in, ring, flags)
+        out = ex.array_data("Out")
+        assert np.array_equal(out.view(np.uint64), want.view(np.uint64))
+        monkeypatch.setenv("PCOTGPU_RESIDENT", "0")
+        r2 = ex.run_untiled()
+        assert r2.bt > 0 and r2.checksum_hex == r.checksum_hex
+
+
+def test_resident_stencil_config0_golden_repeated(monkeypatch):
+    """BASELINE config 0 through the resident kernel, three runs on one
+    executor (flags and exchange lines are re-armed per run; a band-to-band
+    ordering race would show as a flaky checksum)."""
+    monkeypatch.setenv("PCOTGPU_RESIDENT", "1")
+    want = [e["checksum"] for e in O.goldens()
+            if e["kernel"] == "jacobi2d" and e["params"] == {"T": 256, "N": 2048}][0]
+    with P.GpuExecutor("jacobi2d", {"T": 256, "N": 2048}) as ex:
+        for _ in range(3):
+            r = ex.run_untiled()
+            assert r.bt == 0 and r.checksum_hex == want

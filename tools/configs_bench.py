@@ -89,7 +89,7 @@ def main():
                                         "note": "HBM traffic ~1 B/update: F in, Out back, one wrap "
                                                 "buffer round trip per 16 sweeps"}
                 else:
-                    bpu = 16.0 / first.bt
+                    bpu = 16.0 / max(first.bt, 1)
                     line["roofline"] = {"bound": "hbm", "bytes_per_update": bpu, "peak_GBs": hbm,
                                         "achieved_GBs": round(gu * bpu, 1), "frac": round(gu * bpu / hbm, 3)}
                 want = golden(kernel, params)
