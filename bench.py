@@ -634,9 +634,9 @@ def measure_e2e(args, P, torch, dist, S, dev, world, rows, updates, local):
         out_np = host_out.numpy()
         sched = ("slt" if args.scheme == "slt" else "cot", [args.bt, 64, 256])
         ex.run_batch([F_np], [out_np], *sched, skip_checksum=True)  # allocates staging
-        # a 32-instance batch: the first input copy and the last output copy
+        # a 64-instance batch: the first input copy and the last output copy
         # (~0.16 s each at PCIe rates) are the batch's only unoverlapped work
-        steps = max(32, args.steps)
+        steps = max(64, args.steps)
         r = ex.run_batch([F_np] * steps, [out_np] * steps, *sched, skip_checksum=True)
         ms = r.device_ms / steps
         # the batch's output equals a plain run's (first rows compared)
