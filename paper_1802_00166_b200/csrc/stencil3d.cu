@@ -356,8 +356,8 @@ struct Edge3v2 {
 template <int BT, int RULE, bool MASKJK, bool HOLD, class G, int P>
 PCOT_DEV void s3v2_iter(Regs3v2<BT, G>& R, const double* __restrict__ ring, int k, int par,
                         double* __restrict__ edge, int warp, int lane, const S3Args& a,
-                        unsigned jkmask, int i0, int i1, double* __restrict__ obase,
-                        unsigned smask, int jrow0, int j0, int jend) {
+                        unsigned jkmask, int i0, int i1, double* __restrict__ oplane,
+                        unsigned smask, unsigned rmask) {
   constexpr int C = G::C, RJ = G::RJ, KL = G::KL, PF = G::PF, SLOT = G::SLOT;
   constexpr int EW = Edge3v2<BT, G>::EW;
   // ring slots of input planes k-2, k-1, k; this thread's cell (r, c) of
@@ -424,44 +424,46 @@ PCOT_DEV void s3v2_iter(Regs3v2<BT, G>& R, const double* __restrict__ ring, int 
         }
     }
     const bool ringp = rho < 1 || rho > a.n - 2;
+    // computed on every plane, then overridden on the two ring planes (a
+    // warp-uniform, almost never taken branch; an if/else diamond around the
+    // update made the compiler pre-zero all of nv on every plane)
+#pragma unroll
+    for (int r = 0; r < RJ; ++r) {
+      double im[C], ip[C];
+      if constexpr (G::RC) {
+#pragma unroll
+        for (int c = 0; c < C; ++c) {
+          im[c] = R.z[G::RC ? m3(P - 2) : 0][r][c];
+          ip[c] = R.z[G::RC ? m3(P) : 0][r][c];
+        }
+      } else {
+#pragma unroll
+        for (int c = 0; c < C; c += 2) {
+          const double2 u = *reinterpret_cast<const double2*>(p0 + r * KL + c);
+          const double2 w = *reinterpret_cast<const double2*>(p2 + r * KL + c);
+          im[c] = u.x, im[c + 1] = u.y, ip[c] = w.x, ip[c + 1] = w.y;
+        }
+      }
+      const double W = p1[r * KL - 1], E = p1[r * KL + C];
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        const double km = c > 0 ? row[r + 1][c > 0 ? c - 1 : 0] : W;
+        const double kp = c < C - 1 ? row[r + 1][c < C - 1 ? c + 1 : 0] : E;
+        nv[r][c] = update7<RULE>(row[r + 1][c], im[c], ip[c], row[r][c], row[r + 2][c], km, kp);
+      }
+    }
+    if (MASKJK && jkmask != (1u << (RJ * C)) - 1u) {  // only threads with ring cells
+#pragma unroll
+      for (int r = 0; r < RJ; ++r)
+#pragma unroll
+        for (int c = 0; c < C; ++c)
+          if (!((jkmask >> (r * C + c)) & 1u)) nv[r][c] = HOLD ? row[r + 1][c] : 0.0;
+    }
     if (ringp) {
 #pragma unroll
       for (int r = 0; r < RJ; ++r)
 #pragma unroll
         for (int c = 0; c < C; ++c) nv[r][c] = HOLD ? row[r + 1][c] : 0.0;
-    } else {
-#pragma unroll
-      for (int r = 0; r < RJ; ++r) {
-        double im[C], ip[C];
-        if constexpr (G::RC) {
-#pragma unroll
-          for (int c = 0; c < C; ++c) {
-            im[c] = R.z[G::RC ? m3(P - 2) : 0][r][c];
-            ip[c] = R.z[G::RC ? m3(P) : 0][r][c];
-          }
-        } else {
-#pragma unroll
-          for (int c = 0; c < C; c += 2) {
-            const double2 u = *reinterpret_cast<const double2*>(p0 + r * KL + c);
-            const double2 w = *reinterpret_cast<const double2*>(p2 + r * KL + c);
-            im[c] = u.x, im[c + 1] = u.y, ip[c] = w.x, ip[c + 1] = w.y;
-          }
-        }
-        const double W = p1[r * KL - 1], E = p1[r * KL + C];
-#pragma unroll
-        for (int c = 0; c < C; ++c) {
-          const double km = c > 0 ? row[r + 1][c > 0 ? c - 1 : 0] : W;
-          const double kp = c < C - 1 ? row[r + 1][c < C - 1 ? c + 1 : 0] : E;
-          nv[r][c] = update7<RULE>(row[r + 1][c], im[c], ip[c], row[r][c], row[r + 2][c], km, kp);
-        }
-      }
-      if (MASKJK && jkmask != (1u << (RJ * C)) - 1u) {  // only threads with ring cells
-#pragma unroll
-        for (int r = 0; r < RJ; ++r)
-#pragma unroll
-          for (int c = 0; c < C; ++c)
-            if (!((jkmask >> (r * C + c)) & 1u)) nv[r][c] = HOLD ? row[r + 1][c] : 0.0;
-      }
     }
     if (BT > 1) {
       constexpr int s = m3(P);  // level 1's newest plane (k-1) -> slot P
@@ -474,17 +476,16 @@ PCOT_DEV void s3v2_iter(Regs3v2<BT, G>& R, const double* __restrict__ ring, int 
         ecur[(warp + 1) * EW + ((0 * Edge3v2<BT, G>::LV + 0) * 32 + lane) * C + c] = nv[0][c];
         ecur[(warp + 1) * EW + ((1 * Edge3v2<BT, G>::LV + 0) * 32 + lane) * C + c] = nv[RJ - 1][c];
       }
-    } else if (rho >= i0 && rho < i1) {
+    } else if (rho >= i0 && rho < i1 && smask != 0u) {
 #pragma unroll
       for (int r = 0; r < RJ; ++r) {
-        const int j = jrow0 + r;
-        if (j < j0 || j >= jend) continue;
-        double* dst = obase + int64_t(rho) * a.pi_out + int64_t(j) * a.pj_out;
+        if (!((rmask >> r) & 1u)) continue;
+        double* dst = oplane + r * a.pj_out;
         if (smask == (1u << C) - 1u) {
 #pragma unroll
           for (int c = 0; c < C; c += 2)
             __stcs(reinterpret_cast<double2*>(dst + c), make_double2(nv[r][c], nv[r][c + 1]));
-        } else if (smask != 0u) {  // grid-edge tiles only; halo lanes store nothing
+        } else {  // grid-edge tiles only
 #pragma unroll
           for (int c = 0; c < C; ++c)
             if ((smask >> c) & 1u) __stcs(dst + c, nv[r][c]);
@@ -502,36 +503,35 @@ PCOT_DEV void s3v2_iter(Regs3v2<BT, G>& R, const double* __restrict__ ring, int 
     double nv[RJ][C];
     const bool ringp = rho < 1 || rho > a.n - 2;
     prefetch(L + kPFE);
+    // padded: warp 0 / NW-1 read pad rows (halo cells)
+    const double* up = upP[L - 1];
+    const double* dn = dnP[L - 1];
+#pragma unroll
+    for (int r = 0; r < RJ; ++r) {
+      const double W = __shfl_up_sync(0xffffffffu, mid[r][C - 1], 1);
+      const double E = __shfl_down_sync(0xffffffffu, mid[r][0], 1);
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        const double jm = r > 0 ? mid[r > 0 ? r - 1 : 0][c] : up[c];
+        const double jp = r < RJ - 1 ? mid[r < RJ - 1 ? r + 1 : 0][c] : dn[c];
+        const double km = c > 0 ? mid[r][c > 0 ? c - 1 : 0] : W;
+        const double kp = c < C - 1 ? mid[r][c < C - 1 ? c + 1 : 0] : E;
+        nv[r][c] = update7<RULE>(mid[r][c], R.v[L - 1][st][r][c], R.v[L - 1][sb][r][c], jm, jp,
+                                 km, kp);
+      }
+    }
+    if (MASKJK && jkmask != (1u << (RJ * C)) - 1u) {  // only threads with ring cells
+#pragma unroll
+      for (int r = 0; r < RJ; ++r)
+#pragma unroll
+        for (int c = 0; c < C; ++c)
+          if (!((jkmask >> (r * C + c)) & 1u)) nv[r][c] = HOLD ? mid[r][c] : 0.0;
+    }
     if (ringp) {
 #pragma unroll
       for (int r = 0; r < RJ; ++r)
 #pragma unroll
         for (int c = 0; c < C; ++c) nv[r][c] = HOLD ? mid[r][c] : 0.0;
-    } else {
-      // padded: warp 0 / NW-1 read pad rows (halo cells)
-      const double* up = upP[L - 1];
-      const double* dn = dnP[L - 1];
-#pragma unroll
-      for (int r = 0; r < RJ; ++r) {
-        const double W = __shfl_up_sync(0xffffffffu, mid[r][C - 1], 1);
-        const double E = __shfl_down_sync(0xffffffffu, mid[r][0], 1);
-#pragma unroll
-        for (int c = 0; c < C; ++c) {
-          const double jm = r > 0 ? mid[r > 0 ? r - 1 : 0][c] : up[c];
-          const double jp = r < RJ - 1 ? mid[r < RJ - 1 ? r + 1 : 0][c] : dn[c];
-          const double km = c > 0 ? mid[r][c > 0 ? c - 1 : 0] : W;
-          const double kp = c < C - 1 ? mid[r][c < C - 1 ? c + 1 : 0] : E;
-          nv[r][c] = update7<RULE>(mid[r][c], R.v[L - 1][st][r][c], R.v[L - 1][sb][r][c], jm, jp,
-                                   km, kp);
-        }
-      }
-      if (MASKJK && jkmask != (1u << (RJ * C)) - 1u) {  // only threads with ring cells
-#pragma unroll
-        for (int r = 0; r < RJ; ++r)
-#pragma unroll
-          for (int c = 0; c < C; ++c)
-            if (!((jkmask >> (r * C + c)) & 1u)) nv[r][c] = HOLD ? mid[r][c] : 0.0;
-      }
     }
     if (L + 1 < BT) {
       constexpr int dummy = 0;
@@ -546,17 +546,16 @@ PCOT_DEV void s3v2_iter(Regs3v2<BT, G>& R, const double* __restrict__ ring, int 
         ecur[(warp + 1) * EW + ((0 * LV + L) * 32 + lane) * C + c] = nv[0][c];
         ecur[(warp + 1) * EW + ((1 * LV + L) * 32 + lane) * C + c] = nv[RJ - 1][c];
       }
-    } else if (rho >= i0 && rho < i1) {
+    } else if (rho >= i0 && rho < i1 && smask != 0u) {
 #pragma unroll
       for (int r = 0; r < RJ; ++r) {
-        const int j = jrow0 + r;
-        if (j < j0 || j >= jend) continue;
-        double* dst = obase + int64_t(rho) * a.pi_out + int64_t(j) * a.pj_out;
+        if (!((rmask >> r) & 1u)) continue;
+        double* dst = oplane + r * a.pj_out;
         if (smask == (1u << C) - 1u) {
 #pragma unroll
           for (int c = 0; c < C; c += 2)
             __stcs(reinterpret_cast<double2*>(dst + c), make_double2(nv[r][c], nv[r][c + 1]));
-        } else if (smask != 0u) {  // grid-edge tiles only; halo lanes store nothing
+        } else {  // grid-edge tiles only
 #pragma unroll
           for (int c = 0; c < C; ++c)
             if ((smask >> c) & 1u) __stcs(dst + c, nv[r][c]);
@@ -596,7 +595,14 @@ PCOT_DEV void s3v2_tile(const S3Args& a, const CUtensorMap* tmap, int tk, int tj
       const int j = jrow0 + r, kk = kb + c;
       if (j >= 1 && j <= a.n - 2 && kk >= 1 && kk <= a.n - 2) jkmask |= 1u << (r * C + c);
     }
-  double* obase = a.out + kb;
+  // rows this thread stores, and the output plane pointer of the current
+  // iteration's last level (plane k - BT), advanced by one plane per iteration
+  unsigned rmask = 0;
+#pragma unroll
+  for (int r = 0; r < RJ; ++r)
+    if (jrow0 + r >= j0 && jrow0 + r < jend) rmask |= 1u << r;
+  if (rmask == 0u) smask = 0u;
+  double* oplane = a.out + kb + int64_t(kstart - BT) * a.pi_out + int64_t(jrow0) * a.pj_out;
   // plane `pl` into slot pl mod PF: one tensor-TMA box (KL x JL) starting at
   // (column kfirst-2, row jfirst-1); the map's origin is the halo corner
   (void)lo;
@@ -634,7 +640,8 @@ PCOT_DEV void s3v2_tile(const S3Args& a, const CUtensorMap* tmap, int tk, int tj
     const int k = kstart + itp;                                                              \
     mbar_wait(&bars[((k % PF) + PF) % PF], uint32_t(((itp) / PF) & 1));                      \
     s3v2_iter<BT, RULE, MASKJK, HOLD, G, P>(R, ring, k, itp & 1, edge, warp, lane, a, jkmask, \
-                                            i0, i1, obase, smask, jrow0, j0, jend);             \
+                                            i0, i1, oplane, smask, rmask);                     \
+    oplane += a.pi_out;                                                                      \
     __syncthreads();                                                                         \
     if (warp == 0 && itp + PF - 2 < niter) issue(k + PF - 2);                                \
   }
