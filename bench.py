@@ -393,6 +393,19 @@ def per_config(P, torch, dev, local, hbm_peak, reps_ms=1000.0):
                                      "peak": hbm_peak, "unit": "GB/s", "frac": round(gu * bpu / hbm_peak, 3)}
                 want = golden_checksum(kernel, params)
                 e["parity"] = {"golden": want, "got": first.checksum_hex, "match": first.checksum_hex == want}
+                if kernel.startswith("heat3d"):
+                    # the next temporal depth beside the default (fewer bytes per update,
+                    # lower roofline fraction): same run, same clocks, checksum-verified
+                    alt = ex.run("slt", [3, 8, 8, 8])
+                    ts = []
+                    for _ in range(max(5, reps // 4)):
+                        flush.zero_()
+                        torch.cuda.synchronize(dev)
+                        ts.append(ex.run("slt", [3, 8, 8, 8], skip_checksum=True).device_ms)
+                    g3 = upd / (statistics.median(ts) / 1e3) / 1e9
+                    e["depth_tradeoff"] = [{"bt": 3, "GUpd/s": round(g3, 1),
+                                            "hbm_frac": round(g3 * 16.0 / 3 / hbm_peak, 3),
+                                            "checksum_match": alt.checksum_hex == want}]
             cl = clocks.summary()
             e["clocks"] = {"sm_mhz": cl["sm_mhz"], "sm_max_mhz": cl["sm_max_mhz"], "reasons": cl["reasons"],
                            "samples": cl["samples"]}

@@ -354,18 +354,21 @@ struct Edge3v2 {
 };
 
 template <int BT, int RULE, bool MASKJK, bool HOLD, class G, int P>
-PCOT_DEV void s3v2_iter(Regs3v2<BT, G>& R, const double* __restrict__ ring, int k, int par,
+PCOT_DEV void s3v2_iter(Regs3v2<BT, G>& R, const double* __restrict__ ring, int k, int s0, int s1,
+                        int s2, int par,
                         double* __restrict__ edge, int warp, int lane, const S3Args& a,
                         unsigned jkmask, int i0, int i1, double* __restrict__ oplane,
                         unsigned smask, unsigned rmask) {
-  constexpr int C = G::C, RJ = G::RJ, KL = G::KL, PF = G::PF, SLOT = G::SLOT;
+  constexpr int C = G::C, RJ = G::RJ, KL = G::KL, SLOT = G::SLOT;
   constexpr int EW = Edge3v2<BT, G>::EW;
   // ring slots of input planes k-2, k-1, k; this thread's cell (r, c) of
   // plane slot s sits at s*SLOT + (warp*RJ + r + 1)*KL + lane*C + c + 2
   const int tb = (warp * RJ + 1) * KL + lane * C + 2;
-  const double* p0 = ring + (((k - 2) % PF + PF) % PF) * SLOT + tb;
-  const double* p1 = ring + (((k - 1) % PF + PF) % PF) * SLOT + tb;
-  const double* p2 = ring + ((k % PF + PF) % PF) * SLOT + tb;
+  // (s0, s1, s2 = their slots, kept as running counters by the caller: no
+  // modulo per plane)
+  const double* p0 = ring + s0 * SLOT + tb;
+  const double* p1 = ring + s1 * SLOT + tb;
+  const double* p2 = ring + s2 * SLOT + tb;
   const double* eprev = edge + (par ^ 1) * Edge3v2<BT, G>::kPerPar;
   double* ecur = edge + par * Edge3v2<BT, G>::kPerPar;
   // Warp-edge rows of levels >= 1 were published in the previous iteration:
@@ -607,8 +610,7 @@ PCOT_DEV void s3v2_tile(const S3Args& a, const CUtensorMap* tmap, int tk, int tj
   // (column kfirst-2, row jfirst-1); the map's origin is the halo corner
   (void)lo;
   (void)hi;
-  auto issue = [&](int pl) {  // warp 0, lane 0
-    const int slot = ((pl % PF) + PF) % PF;
+  auto issue = [&](int pl, int slot) {  // warp 0, lane 0; slot = pl mod PF
     if (lane == 0) {
       mbar_arrive_expect_tx(&bars[slot], JL * KL * 8);
       tma_load_3d(ring + slot * SLOT, tmap, kfirst - 2 + a.halo, jfirst - 1 + a.halo, pl + a.halo,
@@ -616,8 +618,18 @@ PCOT_DEV void s3v2_tile(const S3Args& a, const CUtensorMap* tmap, int tk, int tj
     }
   };
   // prefetch distance PF-2: slot of plane k+PF-2 held plane k-2, last read at k
+  // running ring state: slots of planes k-2, k-1, k and the phase of plane k's
+  // barrier (a slot is used once every PF iterations).  Depths >= 3 run
+  // 512-thread CTAs at the 128-register cap, where the per-plane modulo
+  // arithmetic cost registers (bt=3: 478 -> 550 GUpd/s with running counters);
+  // the shallower kernels are faster with the modulo in uniform registers
+  // (bt=1: 305 vs 272), so they keep it (profiles/s3d7_r02.md).
+  constexpr bool kRun = BT >= 3;
+  const int sl0 = ((kstart % PF) + PF) % PF;
+  int s2 = sl0, s1 = (sl0 + PF - 1) % PF, s0 = (sl0 + PF - 2) % PF, wrap = 0;
+  uint32_t phase = 0;
   if (warp == 0)
-    for (int it = 0; it < PF - 2 && it < niter; ++it) issue(kstart + it);
+    for (int it = 0; it < PF - 2 && it < niter; ++it) issue(kstart + it, (sl0 + it) % PF);
   Regs3v2<BT, G> R;
 #pragma unroll
   for (int L = 0; L < Edge3v2<BT, G>::LV; ++L)
@@ -638,12 +650,27 @@ PCOT_DEV void s3v2_tile(const S3Args& a, const CUtensorMap* tmap, int tk, int tj
   {                                                                                          \
     const int itp = it + P;                                                                  \
     const int k = kstart + itp;                                                              \
-    mbar_wait(&bars[((k % PF) + PF) % PF], uint32_t(((itp) / PF) & 1));                      \
-    s3v2_iter<BT, RULE, MASKJK, HOLD, G, P>(R, ring, k, itp & 1, edge, warp, lane, a, jkmask, \
-                                            i0, i1, oplane, smask, rmask);                     \
+    int q0, q1, q2;                                                                          \
+    uint32_t ph;                                                                             \
+    if constexpr (kRun) {                                                                    \
+      q0 = s0, q1 = s1, q2 = s2, ph = phase;                                                 \
+    } else {                                                                                 \
+      q0 = (((k - 2) % PF) + PF) % PF, q1 = (((k - 1) % PF) + PF) % PF;                      \
+      q2 = ((k % PF) + PF) % PF, ph = uint32_t((itp / PF) & 1);                              \
+    }                                                                                        \
+    mbar_wait(&bars[q2], ph);                                                                \
+    s3v2_iter<BT, RULE, MASKJK, HOLD, G, P>(R, ring, k, q0, q1, q2, itp & 1, edge, warp, lane, a, \
+                                            jkmask, i0, i1, oplane, smask, rmask);             \
     oplane += a.pi_out;                                                                      \
     __syncthreads();                                                                         \
-    if (warp == 0 && itp + PF - 2 < niter) issue(k + PF - 2);                                \
+    /* plane k+PF-2 goes into the slot that held plane k-2 */                                \
+    if (warp == 0 && itp + PF - 2 < niter) issue(k + PF - 2, q0);                            \
+    if constexpr (kRun) {                                                                    \
+      s0 = s1;                                                                               \
+      s1 = s2;                                                                               \
+      s2 = s2 + 1 == PF ? 0 : s2 + 1;                                                        \
+      if (++wrap == PF) wrap = 0, phase ^= 1u;                                               \
+    }                                                                                        \
   }
     PCOT_S3V2_STEP(0)
     PCOT_S3V2_STEP(1)

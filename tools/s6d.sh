@@ -1,15 +1,11 @@
 o=gpurun_out
 rm -f $o/s6d_*.log
 L=paper_1802_00166_b200/libpcotgpu.so
-for v in A B A B; do
-  cp _exp/lib_$v.so $L
-  echo "lib $v" >> $o/s6d_ab.log
-  timeout 200 python tools/kbench.py s3d7 --bts 2 --reps 150 2>&1 | grep GUpd >> $o/s6d_ab.log
+for lib in B D; do
+  cp _exp/lib_$lib.so $L
+  for v in 28 26 15 24 27; do
+    echo "lib $lib variant $v bt2" >> $o/s6d_ab.log
+    PCOTGPU_S3D7_VARIANT=$v timeout 300 python tools/kbench.py s3d7 --bts 2 --reps 60 2>&1 | grep GUpd >> $o/s6d_ab.log
+  done
 done
-for v in A B; do
-  cp _exp/lib_$v.so $L
-  echo "lib $v bt1 bt3" >> $o/s6d_ab.log
-  timeout 200 python tools/kbench.py s3d7 --bts 1,3 --reps 60 2>&1 | grep GUpd >> $o/s6d_ab.log
-done
-cp _exp/lib_B.so $L
-timeout 900 python -m pytest tests -m gpu -q -x -k "heat3d or s3d7 or 3d" > $o/s6d_t.log 2>&1; echo rc $? >> $o/s6d_t.log
+cp _exp/lib_E.so $L
