@@ -46,7 +46,7 @@ def s2d5(a):
 
             def one():
                 S.advance(0, 1, 0, S.R, bt, torch.cuda.current_stream())
-            ms = ev_time(one)
+            ms = ev_time(one, a.reps)
             print(json.dumps({"kernel": "s2d5", "bt": bt, "order": "slt" if order == 0 else "cot",
                               "ms": round(ms, 4), "GUpd/s": round(cells * bt / ms / 1e6, 1),
                               "GB/s(16B/cell)": round(16 * cells / ms / 1e6, 1)}), flush=True)
