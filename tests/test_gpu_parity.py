@@ -138,6 +138,19 @@ def test_gemm_tolerance(N, scheme):
         _gemm_check(ex.array_data("Out"), N)
 
 
+@pytest.mark.parametrize("variant", [0, 10, 9, 1])
+@pytest.mark.parametrize("N", [2, 15, 130, 257, 1032])
+def test_gemm_kernel_variants_ragged_sizes(monkeypatch, variant, N):
+    """Every DGEMM load path on sizes that are not multiples of the 128x128 CTA
+    tile, the 16-double TMA box or the k-block: the tensor-TMA ring (0: BK 32 x
+    3 stages, 10: BK 16 x 6; out-of-bounds box parts are zero-filled by the TMA
+    engine) and the cp.async kernels of round 1 (9, 1), Morton tile order."""
+    monkeypatch.setenv("PCOTGPU_DGEMM_VARIANT", str(variant))
+    with P.GpuExecutor("gemm", {"N": N}) as ex:
+        ex.run("cot", [16, 16, 16])
+        _gemm_check(ex.array_data("Out"), N)
+
+
 @pytest.mark.parametrize("scheme", ["untiled", "slt"])
 def test_gemm_config3_all_rows(scheme):
     """BASELINE config 3 (N=4096): every one of the 4096 rows against the
