@@ -5,6 +5,8 @@ tests/golden/golden.json was produced by running the UNMODIFIED reference
 tests/golden/make_golden.py.  The oracle must reproduce every checksum bit
 for bit before any GPU parity claim rests on it.
 """
+import os
+
 import numpy as np
 import pytest
 
@@ -50,6 +52,10 @@ def test_oracle_matches_reference_interpreter(e):
 def test_oracle_matches_reference_emitted_c(e):
     if e["kernel"] == "gemm" and e["params"]["N"] > 1024:
         pytest.skip("N=4096 oracle GEMM is exercised on the GPU box (rows subset)")
+    if e["params"].get("N", 0) >= 32768 and not os.environ.get("PCOT_FULL_ORACLE"):
+        # config 4 at full size: 5.5e11 updates, ~5 min on 16 cores and 24 GiB; run with
+        # PCOT_FULL_ORACLE=1 (passes: the oracle reproduces the reference's 2d0b3eb672343d76)
+        pytest.skip("full-size config 4 oracle run: set PCOT_FULL_ORACLE=1")
     out = O.reference_output(e["kernel"], e["params"])
     assert "%016x" % O.fnv1a(out) == e["checksum"]
 
