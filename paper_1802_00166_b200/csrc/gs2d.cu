@@ -802,6 +802,8 @@ __global__ void __launch_bounds__((NW + (H > 1)) * 32, H > 1 ? 2 : 1) gs2d_pipe_
       double* const op = orow + j0;
       double* const ep = eb_mine + j0;
       const unsigned emask = elane ? inb : 0u;
+      auto clocks = [&](auto OUT) {
+      constexpr bool kOut = decltype(OUT)::value;
       static_for<S>([&](auto KK) {
         constexpr int kk = decltype(KK)::value;
         // next chunk's edge values: loaded part-way through this chunk, late
@@ -839,8 +841,16 @@ __global__ void __launch_bounds__((NW + (H > 1)) * 32, H > 1 ? 2 : 1) gs2d_pipe_
         // maps the sentinel pattern to its neighbour NaN — copy_rows_nosentinel;
         // test_gs2d_pipeline_nan_input_with_sentinel_bits)
         st_relaxed_if_at<kk>(ep, v, (emask >> kk) & 1u);
-        st_global_if_at<kk>(op, v, (omask >> kk) & 1u);  // result / wrap buffer
+        // result / wrap buffer: only the last level's warps and the CTA's last
+        // warp store here; the other warps run a body without the predicate
+        // arithmetic and the predicated-off store (4 of 31 instructions)
+        if constexpr (kOut) st_global_if_at<kk>(op, v, (omask >> kk) & 1u);
       });
+      };
+      if (last || w == NW - 1)
+        clocks(std::true_type{});
+      else
+        clocks(std::false_type{});
       PCOT_PROF(5);
 #ifdef PCOT_EDGE_FENCE
       __threadfence();
